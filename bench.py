@@ -1,0 +1,455 @@
+"""Benchmark of the RK4 hot path on B200 (driver contract: one JSON line).
+
+Default workload = BASELINE.json configs[1] ("C2"): 2^20 independent 2-DOF
+systems, fp64, dt=1e-4, 10^4 RK4 steps, seeded synthetic inputs.  One bench
+"step" = one full pass of the hot path over that batch (2.1e10 DOF-steps).
+Metric: DOF-steps/s (whole job, all ranks).  --config C1/C3/C4 times the other
+single-GPU configurations the same way (DESIGN.md lists their lines).
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): C2/C4 are independent systems,
+so every rank integrates its own seeded batch of the full per-GPU size (weak
+scaling, no data-path collective); device time is the max over ranks.
+
+--impl reference times the reference algorithm on the host CPU (the
+byte-identical C restatement in oracle/, all host threads) on a bounded sample
+of the same workload and reports the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1702_02207_b200 import workloads  # noqa: E402
+
+METRIC = "DOF-steps/s"
+UNIT = "DOF-steps/s"
+HBM_BYTES_PER_DOF_STEP = 48  # read x,v,m,C + write x,v, one step per round trip
+FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42}
+# DP-pipe instructions per DOF-step in the kernels (SASS-derived):
+# batch2: 68 +,-,* and 8 divisions x 3 (hoisted reciprocal) per system-step.
+DP_INST_PER_DOF_STEP = {"C1": 46, "C2": 46, "C3": 52, "C4": 52}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str, config: str):
+    """dram bytes per launch from the committed ncu --set full summary, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel, {}).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# workloads: inputs resident in HBM + one "step" of the hot path
+# --------------------------------------------------------------------------
+
+class Workload:
+    def __init__(self, name, rank, device, halo):
+        import torch
+
+        from paper_1702_02207_b200 import batched
+
+        self.name, self.batched, self.torch = name, batched, torch
+        p = workloads.PARAMS[name]
+        self.dt, self.nsteps = p.dt, p.nsteps
+        self.halo = halo
+        if name == "C2":
+            arrays = workloads.c2(rank=rank)
+            self.kernel, self.launches = "batch2_rk4_kernel", 1
+            self.desc = {"workload": "C2: 2^20 independent 2-DOF systems (eq. 2), SoA [2][B]",
+                         "systems_per_gpu": workloads.C2_B}
+        elif name == "C4":
+            arrays = workloads.c4(rank=rank)
+            self.kernel = "chain_rk4_kernel<4>"
+            self.launches = -(-p.nsteps // 512)
+            self.desc = {"workload": "C4: 4096 chains x 1024 cells, [B][s]",
+                         "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
+        elif name == "C3":
+            arrays = workloads.c3()
+            T = halo or 32
+            self.kernel = "chain_rk4_kernel<8>"
+            self.launches = -(-p.nsteps // T)
+            self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",
+                         "cells": workloads.C3_S, "halo_steps": T}
+        elif name == "C1":
+            arrays = workloads.c1()
+            arrays = tuple(a[:, None] for a in arrays)
+            self.kernel, self.launches = "batch2_rk4_kernel", 1
+            self.desc = {"workload": "C1: paper 2-DOF system, C/m=1012.5, 10^6 steps (latency)"}
+        else:
+            raise SystemExit(f"unknown config {name}")
+        self.host = arrays
+        self.dev = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(device) for a in arrays)
+        self.dof = int(arrays[0].size)
+        self.dof_steps = self.dof * self.nsteps
+
+    def step(self):
+        m, C, x0, v0 = self.dev
+        if self.name in ("C2", "C1"):
+            return self.batched.integrate_batch2(m, C, x0, v0, self.dt, self.nsteps, check=False)
+        if self.name == "C3":
+            return self.batched.integrate_chains(m[None], C[None], x0[None], v0[None], self.dt,
+                                                 self.nsteps, check=False,
+                                                 halo_steps=self.halo)
+        return self.batched.integrate_chains(m, C, x0, v0, self.dt, self.nsteps, check=False)
+
+    # ---- end to end through the host-pointer C ABI --------------------------------
+    def e2e(self, steps, warmup):
+        from paper_1702_02207_b200 import _native
+
+        torch = self.torch
+        lib = _native.lib()
+        pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in self.host]
+        m, C, x0, v0 = pinned
+        x = torch.empty_like(x0).pin_memory()
+        v = torch.empty_like(v0).pin_memory()
+        if self.name in ("C2", "C1"):
+            B = x0.shape[1]
+            fb = torch.empty(B, dtype=torch.int64).pin_memory()
+            call = lambda: lib.osc_rk4_batch2_host(  # noqa: E731
+                m.data_ptr(), C.data_ptr(), x.data_ptr(), v.data_ptr(), B, self.dt,
+                self.nsteps, self.nsteps, None, None, fb.data_ptr())
+        else:
+            B, s = (1, x0.numel()) if self.name == "C3" else x0.shape
+            fb = torch.empty(B, dtype=torch.int64).pin_memory()
+            call = lambda: lib.osc_rk4_chains_host(  # noqa: E731
+                m.data_ptr(), C.data_ptr(), x.data_ptr(), v.data_ptr(), B, s, self.dt,
+                self.nsteps, self.nsteps, None, None, fb.data_ptr())
+        h2d = sum(t.numel() * 8 for t in pinned)
+        d2h = 2 * x0.numel() * 8 + fb.numel() * 8
+        times = []
+        for i in range(warmup + steps):
+            x.copy_(x0)
+            v.copy_(v0)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            rc = call()  # synchronous: H2D, kernels, D2H, stream sync
+            dt = time.perf_counter() - t
+            if rc not in (_native.OSC_OK, _native.OSC_NONFINITE):
+                raise RuntimeError(_native.last_error())
+            if i >= warmup:
+                times.append(dt)
+        return sum(times), h2d, d2h
+
+
+def fp64_peak(device_index):
+    """Measured DP-pipe issue rate (lane-instructions/s) with the DFMA microbench."""
+    import torch
+
+    from paper_1702_02207_b200 import _native
+
+    lib = _native.lib()
+    sink = torch.empty(1024, dtype=torch.float64, device=device_index)
+    ops = ctypes.c_int64(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    best = 0.0
+    for it in (2000, 20000, 20000):
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        rc = lib.osc_bench_fp64(it, 0, sink.data_ptr(), ctypes.byref(ops), stream)
+        end.record()
+        torch.cuda.synchronize()
+        if rc:
+            raise RuntimeError(_native.last_error())
+        best = max(best, ops.value / (start.elapsed_time(end) * 1e-3))
+    return best
+
+
+def cpu_baseline(wl: Workload, budget_s: float = 12.0):
+    """Reference algorithm (oracle C restatement, byte-identical to oscbench) on
+    the host cores, on a bounded sample of the same workload."""
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    m, C, x0, v0 = wl.host
+    if wl.name in ("C2", "C1"):
+        B = m.shape[1]
+        # calibrate: a small run, then size the sample for ~budget_s
+        nb = min(B, max(cores * 256, 1024))
+        cal_steps = min(wl.nsteps, 1000)
+        t = time.perf_counter()
+        oracle.c_rk4_batch2_final(m[:, :nb], C[:, :nb], x0[:, :nb], v0[:, :nb], wl.dt, cal_steps)
+        rate = 2 * nb * cal_steps / max(time.perf_counter() - t, 1e-6)
+        nb = int(min(B, max(nb, budget_s * rate / (2 * wl.nsteps))))
+        t = time.perf_counter()
+        oracle.c_rk4_batch2_final(m[:, :nb], C[:, :nb], x0[:, :nb], v0[:, :nb], wl.dt, wl.nsteps)
+        el = time.perf_counter() - t
+        done = 2 * nb * wl.nsteps
+        sample = f"{nb} of {B} systems x {wl.nsteps} steps (full horizon)"
+    elif wl.name == "C4":
+        Bc, s = m.shape
+        nb = max(cores, 8)
+        steps = min(wl.nsteps, 1000)
+        t = time.perf_counter()
+        oracle.c_rk4_chains(m[:nb], C[:nb], x0[:nb], v0[:nb], wl.dt, steps, sample=False)
+        el = time.perf_counter() - t
+        done = nb * s * steps
+        sample = f"{nb} of {Bc} chains x {steps} of {wl.nsteps} steps"
+    else:  # C3: the whole chain, cells split across threads per phase
+        s = m.size
+        steps = 20
+        t = time.perf_counter()
+        oracle.c_rk4_chain_mt(m, C, x0, v0, wl.dt, steps)
+        el = time.perf_counter() - t
+        done = s * steps
+        sample = f"full {s}-cell chain x {steps} of {wl.nsteps} steps"
+    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": sample + " (oracle/rk4_oracle.c, byte-identical to oscbench.integrate)"}
+
+
+# --------------------------------------------------------------------------
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    wl_name = args.config
+    import oracle  # noqa: F401  (the reference arm is the CPU restatement)
+
+    class HostOnly:
+        pass
+
+    wl = HostOnly()
+    wl.name = wl_name
+    p = workloads.PARAMS[wl_name]
+    wl.dt, wl.nsteps = p.dt, p.nsteps
+    wl.host = {"C2": workloads.c2, "C4": workloads.c4, "C3": workloads.c3,
+               "C1": lambda: tuple(a[:, None] for a in workloads.c1())}[wl_name]()
+    budget = args.ref_budget
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        last = cpu_baseline(wl, budget_s=budget)
+        if i >= args.warmup:
+            vals.append(last["value"])
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy PCG64, workloads.py)",
+        "config": {"workload": wl_name},
+        "cpu_baseline": dict(last, value=value),
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--halo", type=int, default=0, help="C3 steps per tiled launch")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=8.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: at least 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    if world > 1 and args.config in ("C1", "C3"):
+        raise SystemExit(f"{args.config} is single-GPU in this build (DESIGN.md 'Multi-GPU')")
+
+    wl = Workload(args.config, rank, device, args.halo)
+    fp64 = fp64_peak(local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > L2 (126 MB)
+
+    for _ in range(args.warmup):
+        wl.step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps, outside the step's events
+            starts[i].record()
+            wl.step()
+            ends[i].record()
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    dev_s = sum(step_ms) * 1e-3
+    if world > 1:
+        t = torch.tensor([dev_s], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+
+    e2e = None
+    if not args.no_e2e:
+        e2e_s, h2d, d2h = wl.e2e(max(1, min(args.steps, 5)), 1)
+        n_e2e = max(1, min(args.steps, 5))
+        if world > 1:
+            t = torch.tensor([e2e_s], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * wl.dof_steps * n_e2e / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "timing": "wall clock around the synchronous host-pointer C-ABI call "
+                         "(pinned host buffers; H2D + kernels + D2H inside)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(wl)
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    value = world * wl.dof_steps * args.steps / dev_s
+    per_gpu = wl.dof_steps * args.steps / dev_s
+    launch_s = dev_s / (args.steps * wl.launches)
+    hbm_peak, hbm_src = peaks()
+    alg_bytes = HBM_BYTES_PER_DOF_STEP * wl.dof_steps / wl.launches
+    achieved = alg_bytes / launch_s / 1e9
+    traffic = ncu_traffic(wl.kernel, wl.name)
+    dp_inst_rate = per_gpu * DP_INST_PER_DOF_STEP[wl.name]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy PCG64, workloads.py; no dataset exists)",
+        "config": dict(wl.desc, dt=wl.dt, nsteps_per_step=wl.nsteps,
+                       dof_steps_per_gpu_step=wl.dof_steps, parallelism=f"dp{world}",
+                       l2="flushed between timed steps (256 MiB memset outside step events); "
+                          "state is register-resident within a step",
+                       arithmetic="IEEE fp64, byte-identical to oscbench.integrate"),
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": traffic,
+            "kernel": wl.kernel, "launches_per_step": wl.launches,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "note": f"SURVEY 8d: 48 B per DOF-step (one step per HBM round trip); peak "
+                    f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
+                    f"is expected; its real limit is the FP64 pipe (roofline_fp64)",
+        },
+        "roofline_fp64": {
+            "bound": "fp64_pipe", "dp_inst_per_dof_step": DP_INST_PER_DOF_STEP[wl.name],
+            "achieved_dp_inst_per_s": dp_inst_rate, "peak_dp_inst_per_s": fp64,
+            "frac": dp_inst_rate / fp64 if fp64 else None,
+            "algorithmic_flops_per_dof_step": FLOPS_PER_DOF_STEP[wl.name],
+            "achieved_flops": per_gpu * FLOPS_PER_DOF_STEP[wl.name],
+            "peak_note": "measured DFMA issue microbenchmark (osc_bench_fp64), lane-inst/s",
+        },
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": wl.launches * args.steps,
+        "clocks": clocks.summary(),
+        "step_ms": step_ms,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

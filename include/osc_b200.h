@@ -1,0 +1,119 @@
+/*
+ * osc_b200.h -- C ABI of the B200-native RK4 oscillator integrator.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   integrate(system, state0, dt, nsteps, stride)  oscbench/oscillator.py:234-263
+ *   rk4_step(system, state, dt)                     oscbench/oscillator.py:194-231
+ * The reference is a pure-Python package with no FFI of its own;
+ * INTEGRATION.md shows the ctypes binding a maintainer would add to it and
+ * paper_1702_02207_b200/_native.py is that binding.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes; no C++ exception crosses the ABI.
+ *   - Status codes: OSC_OK, OSC_NONFINITE (host API only: some system
+ *     diverged, see first_bad), OSC_INVALID (bad argument -- the reference's
+ *     ValueError: dt not finite/positive (oscillator.py:201-202), nsteps < 1 or
+ *     stride < 1 (:247-250)), OSC_CUDA_ERROR.  osc_last_error() returns the
+ *     calling thread's last message.
+ *   - Device API: all pointers are device pointers, work is enqueued on
+ *     `stream` (a cudaStream_t; NULL = legacy default stream) and the call
+ *     returns without synchronising.  Host API (*_host): host pointers,
+ *     synchronous, host<->device copies inside.
+ *   - first_bad[b] receives the 1-based step at which system/chain b first
+ *     produced a NaN or infinity (NonFiniteStateError.step,
+ *     oscillator.py:255-260), or 0.  After divergence the final state of that
+ *     system is unspecified (the reference raises instead of returning it);
+ *     samples before the bad step are exact.
+ *   - Samples: xs/vs (may be NULL) receive the initial state plus every
+ *     stride-th state, 1 + nsteps/stride slots of the state layout -- the
+ *     reference Trajectory's retention rule (oscillator.py:252, 261-262).
+ *     Time labels are not produced on the device: the host accumulates
+ *     t += dt exactly as the reference does (oscillator.py:231).
+ *   - All arithmetic is IEEE binary64 in the reference's operation order:
+ *     results are byte-identical to oscbench.integrate.
+ */
+#ifndef OSC_B200_H
+#define OSC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSC_OK 0
+#define OSC_NONFINITE 1
+#define OSC_INVALID 2
+#define OSC_CUDA_ERROR 3
+
+#define OSC_ABI_VERSION 1
+
+int osc_abi_version(void);
+const char *osc_last_error(void);
+
+/* Batched independent 2-DOF systems (paper eq. 2), SoA layout [2][B]:
+ * m, C, x, v hold coordinate 0 of all B systems, then coordinate 1.
+ * Replaces integrate() for s = 2 (oscillator.py:234-263).
+ * xs/vs: [1 + nsteps/stride][2][B].  first_bad: [B]. */
+int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
+                   double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                   int64_t *first_bad, void *stream);
+
+/* B independent wall-anchored chains of s cells, layout [B][s]
+ * (spring i joins cell i to cell i-1, spring 0 to the wall, last cell free;
+ * oscillator.py:3-5, 152-164).  Chains up to 2048 cells run one CTA per chain
+ * for the whole run; longer chains use temporally blocked tiles of
+ * halo_steps steps per launch (0 = default 32).
+ * Replaces integrate() (oscillator.py:234-263).
+ * xs/vs: [1 + nsteps/stride][B][s].  first_bad: [B]. */
+int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B,
+                   int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                   int64_t *first_bad, int64_t halo_steps, void *stream);
+
+/* One temporally blocked launch over a chain shard buffer of n cells, used by
+ * the multi-GPU driver: cells [own_lo, own_hi) are advanced nsteps steps from
+ * (xin, vin) into (xout, vout); the cells outside are ghosts copied from the
+ * neighbouring shards.  Buffer cell 0 is treated as wall-adjacent and cell
+ * n-1 as the free end, which is exact at the true chain ends and, elsewhere,
+ * harmless as long as each ghost zone is at least 2*nsteps cells wide.
+ * first_bad: [1], updated to the minimum bad step (global step0 + j). */
+int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
+                          const double *vin, double *xout, double *vout, int64_t n,
+                          int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
+                          int64_t step0, int64_t *first_bad, void *stream);
+
+/* derivative() (oscillator.py:184-191): dvel[b][i] = acceleration_at(...).
+ * cell_major != 0 selects the [s][B] layout (batched 2-DOF SoA). */
+int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,
+                   int64_t s, int cell_major, void *stream);
+
+/* energy() (oscillator.py:266-276), exact sequential index-order sum per chain. */
+int osc_energy(const double *m, const double *C, const double *x, const double *v, double *out,
+               int64_t B, int64_t s, int cell_major, void *stream);
+
+/* Self-test of the hoisted-reciprocal division against IEEE div.rn.f64 on n
+ * random operand pairs (mode 0: masses in [0.5,2), any numerator; 1: any
+ * positive divisor; 2: physical ranges).  Synchronous; *mismatches (host)
+ * receives the number of pairs whose bits differ. */
+int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream);
+
+/* FP64 pipe microbenchmark (roofline denominator; not part of the hot path):
+ * enqueues one launch of 8 independent DFMA (mode 0) or DADD (mode 1)
+ * chains per thread; *lane_ops (host) = DP lane-instructions it executes.
+ * sink: device scratch of >= 512 doubles. */
+int osc_bench_fp64(int64_t iters, int mode, double *sink, int64_t *lane_ops, void *stream);
+
+/* Host-pointer convenience forms: synchronous, copies inside, return
+ * OSC_NONFINITE when any system diverged. */
+int osc_rk4_batch2_host(const double *m, const double *C, double *x, double *v, int64_t B,
+                        double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                        int64_t *first_bad);
+int osc_rk4_chains_host(const double *m, const double *C, double *x, double *v, int64_t B,
+                        int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs,
+                        double *vs, int64_t *first_bad);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSC_B200_H */

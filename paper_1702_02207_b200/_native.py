@@ -1,0 +1,83 @@
+"""ctypes binding of ``libosc_b200.so`` (declared in ``include/osc_b200.h``).
+
+This is the binding a maintainer would add to the reference package (see
+INTEGRATION.md).  There is no CPU fallback: if the library or a CUDA device is
+missing, every entry point raises :class:`NativeUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libosc_b200.so")
+
+OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
+ABI_VERSION = 1
+
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_dbl = ctypes.c_double
+
+# name -> (restype, argtypes); mirrors include/osc_b200.h one to one.
+SIGNATURES = {
+    "osc_abi_version": (ctypes.c_int, []),
+    "osc_last_error": (ctypes.c_char_p, []),
+    "osc_rk4_batch2": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp, _vp,
+                                      _vp, _vp]),
+    "osc_rk4_chains": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64, _vp,
+                                      _vp, _vp, _i64, _vp]),
+    "osc_rk4_chain_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                             _dbl, _i64, _i64, _vp, _vp]),
+    "osc_derivative": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
+    "osc_energy": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
+    "osc_check_division": (ctypes.c_int, [_i64, ctypes.c_uint64, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_uint64), _vp]),
+    "osc_bench_fp64": (ctypes.c_int, [_i64, ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int64),
+                                       _vp]),
+    "osc_rk4_batch2_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,
+                                           _vp, _vp]),
+    "osc_rk4_chains_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64,
+                                           _vp, _vp, _vp]),
+}
+
+
+class NativeUnavailableError(RuntimeError):
+    """The sm_100a library or a CUDA device is missing; there is no fallback."""
+
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the library and bind every exported symbol (no device needed)."""
+    global _LIB
+    if _LIB is not None and path == LIB_PATH:
+        return _LIB
+    if not os.path.exists(path):
+        raise NativeUnavailableError(
+            f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.osc_abi_version() != ABI_VERSION:
+        raise NativeUnavailableError("libosc_b200.so ABI version mismatch")
+    if path == LIB_PATH:
+        _LIB = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    """The library, after checking a CUDA device is present."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device: the B200 path has no CPU fallback")
+    return load()
+
+
+def last_error() -> str:
+    return (load().osc_last_error() or b"").decode(errors="replace")

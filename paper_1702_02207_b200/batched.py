@@ -1,0 +1,182 @@
+"""Array API over the C ABI: batches of systems and chains resident in HBM.
+
+Inputs may be numpy arrays (copied to the current CUDA device) or float64
+CUDA tensors (used in place when contiguous).  Work is enqueued on the current
+torch stream; results are device tensors.  These are the calls the bench and
+the multi-GPU driver make; ``oscillator.integrate`` is the drop-in wrapper.
+
+    integrate_batch2   BASELINE configs 0-1  (K1 batch2_rk4)
+    integrate_chains   BASELINE configs 2-3  (K2 whole-chain / K3 tiled)
+    chain_advance      one temporally blocked launch over a shard (K3)
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .oscillator import NonFiniteStateError, accumulated_times
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev(a, device=None) -> torch.Tensor:
+    """Contiguous float64 CUDA tensor (no copy when already one)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+        if not t.is_cuda:
+            t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
+            device or torch.device("cuda", torch.cuda.current_device()))
+    if t.dtype != torch.float64:
+        raise TypeError(f"expected float64, got {t.dtype}")
+    return t.contiguous()
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def raise_for(rc: int, what: str):
+    """Map an OSC_* status to the reference's exception types."""
+    if rc == _native.OSC_OK:
+        return
+    msg = f"{what}: {_native.last_error()}"
+    if rc == _native.OSC_INVALID:
+        raise ValueError(msg)
+    if rc == _native.OSC_NONFINITE:
+        raise NonFiniteStateError(msg)
+    raise RuntimeError(msg)
+
+
+@dataclass
+class BatchResult:
+    """Final state, optional samples and per-system first bad step (device)."""
+
+    x: torch.Tensor
+    v: torch.Tensor
+    xs: torch.Tensor | None
+    vs: torch.Tensor | None
+    first_bad: torch.Tensor
+    dt: float
+    nsteps: int
+    stride: int
+    t0: float = 0.0
+
+    def times(self) -> np.ndarray:
+        return accumulated_times(self.t0, self.dt, self.nsteps, self.stride)
+
+    def check(self):
+        """Raise NonFiniteStateError(step=earliest) if any system diverged."""
+        if self.first_bad.numel() == 0:
+            return self
+        fb = self.first_bad
+        nz = fb[fb > 0]
+        if nz.numel():
+            step = int(nz.min().item())
+            idx = int(torch.nonzero(fb == step)[0, 0].item())
+            raise NonFiniteStateError(
+                f"integration diverged at step {step} (system {idx})", step=step)
+        return self
+
+
+def _outputs(x0, v0, nsteps, stride, sample):
+    x = x0.clone()
+    v = v0.clone()
+    xs = vs = None
+    if sample:
+        nsamp = 1 + nsteps // stride
+        xs = torch.empty((nsamp,) + tuple(x0.shape), dtype=torch.float64, device=x0.device)
+        vs = torch.empty_like(xs)
+    return x, v, xs, vs
+
+
+def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, stream=None,
+                     check=True) -> BatchResult:
+    """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2)."""
+    lib = _native.lib()
+    stride = nsteps if stride is None else stride
+    m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
+    if m.dim() != 2 or m.shape[0] != 2 or not (m.shape == C.shape == x0.shape == v0.shape):
+        raise ValueError(f"expected [2][B] arrays, got {tuple(m.shape)}")
+    B = m.shape[1]
+    x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
+    fb = torch.zeros(B, dtype=torch.int64, device=m.device)
+    rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt),
+                                      int(nsteps), int(stride), _ptr(xs), _ptr(vs), _ptr(fb),
+                                      ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_rk4_batch2")
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride))
+    return res.check() if check else res
+
+
+def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, halo_steps=0,
+                     stream=None, check=True) -> BatchResult:
+    """B wall-anchored chains of s cells, ``[B][s]`` (oscillator.py:152-263)."""
+    lib = _native.lib()
+    stride = nsteps if stride is None else stride
+    m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
+    if m.dim() == 1:
+        m, C, x0, v0 = (a[None] for a in (m, C, x0, v0))
+    if not (m.shape == C.shape == x0.shape == v0.shape) or m.dim() != 2:
+        raise ValueError(f"expected [B][s] arrays, got {tuple(m.shape)}")
+    B, s = m.shape
+    x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
+    fb = torch.zeros(B, dtype=torch.int64, device=m.device)
+    rc = lib.osc_rk4_chains(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, s, float(dt),
+                                      int(nsteps), int(stride), _ptr(xs), _ptr(vs), _ptr(fb),
+                                      int(halo_steps), ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_rk4_chains")
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride))
+    return res.check() if check else res
+
+
+def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
+                  stream=None):
+    """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance)."""
+    rc = _native.lib().osc_rk4_chain_advance(
+        _ptr(m), _ptr(C), _ptr(xin), _ptr(vin), _ptr(xout), _ptr(vout), m.numel(), int(own_lo),
+        int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad),
+        ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_rk4_chain_advance")
+
+
+def derivative_chains(m, C, x, *, cell_major=False, stream=None) -> torch.Tensor:
+    """dvel per cell (oscillator.py:184-191); [B][s] or, cell_major, [s][B]."""
+    lib = _native.lib()
+    m, C, x = (_dev(a) for a in (m, C, x))
+    B, s = (x.shape[1], x.shape[0]) if cell_major else x.shape
+    out = torch.empty_like(x)
+    rc = lib.osc_derivative(_ptr(m), _ptr(C), _ptr(x), _ptr(out), B, s,
+                                      int(cell_major), ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_derivative")
+    return out
+
+
+def energy_chains(m, C, x, v, *, cell_major=False, stream=None) -> torch.Tensor:
+    """Exact sequential energy per chain (oscillator.py:266-276) -> [B]."""
+    lib = _native.lib()
+    m, C, x, v = (_dev(a) for a in (m, C, x, v))
+    B, s = (x.shape[1], x.shape[0]) if cell_major else x.shape
+    out = torch.empty(B, dtype=torch.float64, device=x.device)
+    rc = lib.osc_energy(_ptr(m), _ptr(C), _ptr(x), _ptr(v), _ptr(out), B, s,
+                                  int(cell_major), ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_energy")
+    return out
+
+
+def check_division(n: int, seed: int = 1, mode: int = 0) -> int:
+    """Bitwise mismatches of the hoisted-reciprocal division vs div.rn.f64."""
+    out = ctypes.c_uint64(0)
+    rc = _native.lib().osc_check_division(int(n), int(seed), int(mode), ctypes.byref(out),
+                                          ctypes.c_void_p(_stream()))
+    raise_for(rc, "osc_check_division")
+    return int(out.value)

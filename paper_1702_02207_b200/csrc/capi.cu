@@ -1,0 +1,366 @@
+// C-ABI layer: argument validation, launch planning and host-pointer forms.
+// Declarations and conventions: include/osc_b200.h.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/osc_b200.h"
+#include "osc_kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where)
+{
+    return fail(OSC_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define OSC_CUDA(call)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return cuda_fail(e_, #call);                                                    \
+    } while (0)
+
+// The reference's argument checks: rk4_step's dt (oscillator.py:201-202) and
+// integrate's nsteps/stride (oscillator.py:247-250).
+int check_run_args(double dt, int64_t nsteps, int64_t stride)
+{
+    if (!(std::isfinite(dt) && dt > 0.0))
+        return fail(OSC_INVALID, "dt must be positive and finite, got %.17g", dt);
+    if (nsteps < 1)
+        return fail(OSC_INVALID, "nsteps must be >= 1, got %lld", (long long)nsteps);
+    if (stride < 1)
+        return fail(OSC_INVALID, "stride must be >= 1, got %lld", (long long)stride);
+    return OSC_OK;
+}
+
+osc::StepConsts consts(double dt)
+{
+    // Exactly the reference's constants: half_dt = 0.5 * dt (oscillator.py:208)
+    // and dt / 6.0 inside combine_value (oscillator.py:174).
+    return osc::StepConsts{dt, 0.5 * dt, dt / 6.0};
+}
+
+constexpr int64_t kWholeChainMax = 2048;  // 256 threads x 8 cells
+constexpr int64_t kWholeChainSteps = 512; // steps per launch in whole-chain mode
+constexpr int kTileK = 8, kTileThreads = 256;
+constexpr int64_t kTile = int64_t(kTileK) * kTileThreads;
+constexpr int64_t kDefaultHaloSteps = 32;
+
+void pick_whole(int64_t s, int &K, int &threads)
+{
+    // Fewest cells per thread that keep the CTA at <= 256 threads (the
+    // kernel's register budget allows 256 threads up to K = 8).
+    K = 8;
+    for (int k : {1, 2, 4, 8}) {
+        if ((s + k - 1) / k <= 256) {
+            K = k;
+            break;
+        }
+    }
+    const int64_t t = (s + K - 1) / K;
+    threads = static_cast<int>(((t + 31) / 32) * 32);
+}
+
+struct Scratch {
+    double *p = nullptr;
+    cudaStream_t s = nullptr;
+    ~Scratch()
+    {
+        if (p)
+            cudaFreeAsync(p, s);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int osc_abi_version(void) { return OSC_ABI_VERSION; }
+
+const char *osc_last_error(void) { return g_last_error.c_str(); }
+
+int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B, double dt,
+                   int64_t nsteps, int64_t stride, double *xs, double *vs, int64_t *first_bad,
+                   void *stream)
+{
+    if (int rc = check_run_args(dt, nsteps, stride))
+        return rc;
+    if (B < 0)
+        return fail(OSC_INVALID, "B must be >= 0");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
+        return fail(OSC_INVALID, "null buffer");
+    cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs,
+                                       first_bad, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "batch2_rk4_kernel");
+}
+
+int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B, int64_t s,
+                   double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                   int64_t *first_bad, int64_t halo_steps, void *stream_)
+{
+    if (int rc = check_run_args(dt, nsteps, stride))
+        return rc;
+    if (B < 0 || s < 1)
+        return fail(OSC_INVALID, "need B >= 0 and s >= 1 (got B=%lld s=%lld)", (long long)B,
+                    (long long)s);
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
+        return fail(OSC_INVALID, "null buffer");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const int64_t cells = B * s;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(cells);
+
+    osc::SegArgs g{};
+    g.m = m;
+    g.C = C;
+    g.first_bad = first_bad;
+    g.n = s;
+    g.nbuf = B;
+    g.own_lo = 0;
+    g.own_hi = s;
+    g.k = consts(dt);
+    int K = kTileK, threads = kTileThreads;
+    int64_t per_launch;
+    if (s <= kWholeChainMax) {
+        pick_whole(s, K, threads);
+        g.W = s;
+        g.H = 0;
+        g.tiles = 1;
+        per_launch = kWholeChainSteps;
+    } else {
+        const int64_t T = halo_steps > 0 ? halo_steps : kDefaultHaloSteps;
+        g.H = 2 * T;
+        g.W = kTile - 2 * g.H;
+        if (g.W < 1)
+            return fail(OSC_INVALID, "halo_steps=%lld too deep for a %lld-cell tile",
+                        (long long)T, (long long)kTile);
+        g.tiles = (s + g.W - 1) / g.W;
+        per_launch = T;
+    }
+
+    OSC_CUDA(cudaMemsetAsync(first_bad, 0, sizeof(int64_t) * B, stream));
+    if (xs) {
+        OSC_CUDA(cudaMemcpyAsync(xs, x, bytes, cudaMemcpyDeviceToDevice, stream));
+        OSC_CUDA(cudaMemcpyAsync(vs, v, bytes, cudaMemcpyDeviceToDevice, stream));
+    }
+    Scratch scratch;
+    scratch.s = stream;
+    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch.p), 2 * bytes, stream));
+    double *cx = x, *cv = v, *nx = scratch.p, *nv = scratch.p + cells;
+    for (int64_t k0 = 0; k0 < nsteps;) {
+        int64_t n = nsteps - k0;
+        if (n > per_launch)
+            n = per_launch;
+        const int64_t next_sample = (k0 / stride + 1) * stride;
+        if (next_sample - k0 < n)
+            n = next_sample - k0;
+        g.xin = cx;
+        g.vin = cv;
+        g.xout = nx;
+        g.vout = nv;
+        g.nsteps = n;
+        g.step0 = k0;
+        const bool sample = xs && (k0 + n) % stride == 0;
+        g.xs = sample ? xs + ((k0 + n) / stride) * cells : nullptr;
+        g.vs = sample ? vs + ((k0 + n) / stride) * cells : nullptr;
+        cudaError_t e = osc::launch_chain(g, K, threads, stream);
+        if (e != cudaSuccess)
+            return cuda_fail(e, "chain_rk4_kernel");
+        std::swap(cx, nx);
+        std::swap(cv, nv);
+        k0 += n;
+    }
+    if (cx != x) {
+        OSC_CUDA(cudaMemcpyAsync(x, cx, bytes, cudaMemcpyDeviceToDevice, stream));
+        OSC_CUDA(cudaMemcpyAsync(v, cv, bytes, cudaMemcpyDeviceToDevice, stream));
+    }
+    return OSC_OK;
+}
+
+int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, const double *vin,
+                          double *xout, double *vout, int64_t n, int64_t own_lo, int64_t own_hi,
+                          double dt, int64_t nsteps, int64_t step0, int64_t *first_bad,
+                          void *stream)
+{
+    if (int rc = check_run_args(dt, nsteps, 1))
+        return rc;
+    if (n < 1 || own_lo < 0 || own_hi > n || own_lo >= own_hi)
+        return fail(OSC_INVALID, "bad shard range [%lld,%lld) of %lld", (long long)own_lo,
+                    (long long)own_hi, (long long)n);
+    if (!m || !C || !xin || !vin || !xout || !vout || !first_bad)
+        return fail(OSC_INVALID, "null buffer");
+    osc::SegArgs g{};
+    g.m = m;
+    g.C = C;
+    g.xin = xin;
+    g.vin = vin;
+    g.xout = xout;
+    g.vout = vout;
+    g.first_bad = first_bad;
+    g.n = n;
+    g.nbuf = 1;
+    g.own_lo = own_lo;
+    g.own_hi = own_hi;
+    g.H = 2 * nsteps;
+    g.W = kTile - 2 * g.H;
+    if (g.W < 1)
+        return fail(OSC_INVALID, "nsteps=%lld too deep for a %lld-cell tile", (long long)nsteps,
+                    (long long)kTile);
+    g.tiles = (own_hi - own_lo + g.W - 1) / g.W;
+    g.k = consts(dt);
+    g.nsteps = nsteps;
+    g.step0 = step0;
+    cudaError_t e = osc::launch_chain(g, kTileK, kTileThreads, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "chain_rk4_kernel");
+}
+
+int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,
+                   int64_t s, int cell_major, void *stream)
+{
+    if (B < 0 || s < 1)
+        return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    cudaError_t e = osc::launch_derivative(m, C, x, dvel, B, s, cell_major != 0,
+                                           static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "derivative_kernel");
+}
+
+int osc_energy(const double *m, const double *C, const double *x, const double *v, double *out,
+               int64_t B, int64_t s, int cell_major, void *stream)
+{
+    if (B < 0 || s < 1)
+        return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    cudaError_t e = osc::launch_energy(m, C, x, v, out, B, s, cell_major != 0,
+                                       static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "energy_kernel");
+}
+
+int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream_)
+{
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    unsigned long long *d = nullptr;
+    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d), sizeof *d, stream));
+    OSC_CUDA(cudaMemsetAsync(d, 0, sizeof *d, stream));
+    cudaError_t e = osc::launch_check_division(n, seed, mode, d, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "check_division_kernel");
+    unsigned long long h = 0;
+    OSC_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, stream));
+    OSC_CUDA(cudaFreeAsync(d, stream));
+    OSC_CUDA(cudaStreamSynchronize(stream));
+    *mismatches = h;
+    return OSC_OK;
+}
+
+int osc_bench_fp64(int64_t iters, int mode, double *sink, int64_t *lane_ops, void *stream)
+{
+    if (iters < 1 || !sink || !lane_ops)
+        return fail(OSC_INVALID, "bad fp64 bench arguments");
+    cudaError_t e = osc::launch_fp64_peak(iters, mode, sink, lane_ops,
+                                          static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "fp64_peak_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Host-pointer forms: the end-to-end path a CPU caller (the reference's own
+// Python objects via ctypes) uses.  One cudaMemcpyAsync per buffer.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf()
+    {
+        if (p)
+            cudaFree(p);
+    }
+};
+
+int host_run(bool chains, const double *m, const double *C, double *x, double *v, int64_t B,
+             int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+             int64_t *first_bad)
+{
+    if (int rc = check_run_args(dt, nsteps, stride))
+        return rc;
+    if (B < 0 || s < 1)
+        return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
+        return fail(OSC_INVALID, "null buffer");
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t cells = static_cast<size_t>(B * s);
+    const size_t bytes = cells * sizeof(double);
+    const size_t nsamp = xs ? static_cast<size_t>(1 + nsteps / stride) : 0;
+    DevBuf buf;
+    const size_t total = 4 * bytes + B * sizeof(int64_t) + 2 * nsamp * bytes;
+    OSC_CUDA(cudaMalloc(&buf.p, total));
+    double *dm = static_cast<double *>(buf.p), *dC = dm + cells, *dx = dC + cells,
+           *dv = dx + cells;
+    int64_t *dfb = reinterpret_cast<int64_t *>(dv + cells);
+    double *dxs = xs ? reinterpret_cast<double *>(dfb + B) : nullptr;
+    double *dvs = xs ? dxs + nsamp * cells : nullptr;
+    OSC_CUDA(cudaMemcpyAsync(dm, m, bytes, cudaMemcpyHostToDevice, st));
+    OSC_CUDA(cudaMemcpyAsync(dC, C, bytes, cudaMemcpyHostToDevice, st));
+    OSC_CUDA(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, st));
+    OSC_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, st));
+    int rc = chains ? osc_rk4_chains(dm, dC, dx, dv, B, s, dt, nsteps, stride, dxs, dvs, dfb, 0,
+                                     st)
+                    : osc_rk4_batch2(dm, dC, dx, dv, B, dt, nsteps, stride, dxs, dvs, dfb, st);
+    if (rc != OSC_OK)
+        return rc;
+    OSC_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, st));
+    OSC_CUDA(cudaMemcpyAsync(v, dv, bytes, cudaMemcpyDeviceToHost, st));
+    OSC_CUDA(cudaMemcpyAsync(first_bad, dfb, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (xs) {
+        OSC_CUDA(cudaMemcpyAsync(xs, dxs, nsamp * bytes, cudaMemcpyDeviceToHost, st));
+        OSC_CUDA(cudaMemcpyAsync(vs, dvs, nsamp * bytes, cudaMemcpyDeviceToHost, st));
+    }
+    OSC_CUDA(cudaStreamSynchronize(st));
+    int64_t worst = -1;
+    for (int64_t b = 0; b < B; ++b)
+        if (first_bad[b] != 0 && (worst < 0 || first_bad[b] < first_bad[worst]))
+            worst = b;
+    if (worst >= 0)
+        return fail(OSC_NONFINITE, "integration diverged at step %lld (system %lld)",
+                    (long long)first_bad[worst], (long long)worst);
+    return OSC_OK;
+}
+
+}  // namespace
+
+int osc_rk4_batch2_host(const double *m, const double *C, double *x, double *v, int64_t B,
+                        double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                        int64_t *first_bad)
+{
+    return host_run(false, m, C, x, v, B, 2, dt, nsteps, stride, xs, vs, first_bad);
+}
+
+int osc_rk4_chains_host(const double *m, const double *C, double *x, double *v, int64_t B,
+                        int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs,
+                        double *vs, int64_t *first_bad)
+{
+    return host_run(true, m, C, x, v, B, s, dt, nsteps, stride, xs, vs, first_bad);
+}
+
+}  // extern "C"

@@ -1,0 +1,241 @@
+// K2/K3 chain_rk4: wall-anchored spring chains (BASELINE configs 2-3).
+//
+// Restates rk4_step (oscillator.py:194-231) for a chain of n cells, spring i
+// joining cell i to cell i-1, spring 0 to the wall, the last cell free
+// (oscillator.py:3-5, 152-164).  One CTA owns a TILE of blockDim*K
+// contiguous cells, K per thread, all in registers; the four stage
+// evaluations of a step exchange one neighbour position per thread edge
+// (warp shuffles inside a warp, a double-buffered shared-memory slot plus one
+// __syncthreads between warps -- the on-chip form of the reference engine's
+// per-stage StageBarrier, parallel.py:174-255).
+//
+// Two launch shapes use the same kernel:
+//   * whole-chain (K2, config 3): the tile is the whole chain (H = 0), so
+//     both ends are the true wall / free end.
+//   * temporally blocked (K3, config 2): tiles own W cells plus an H = 2T
+//     halo each side and advance T steps per launch.  A step's dependency
+//     radius is 2 cells of x and v, so after T steps the owned
+//     cells are exact; tile edges that are not chain ends are treated as a
+//     wall / free end, and the garbage this creates never reaches the owned
+//     cells.  Ping-pong buffers: each launch reads (xin,vin) and writes only
+//     owned cells of (xout,vout).
+//
+// Forces: f_i = C_i*d_i with d_i = x_i - x_{i-1} (d_0 = x_0 - 0.0 == x_0);
+//   a_i = (f_{i+1} - f_i)/m_i, last cell a = (-f_i)/m_i.  This is the
+//   reference's RN(RN(-C_i*left) + RN(C_{i+1}*(x_{i+1}-x_i)))/m_i term for
+//   term, since (-C)*d == -(C*d) exactly and IEEE addition commutes.
+#include "osc_device.cuh"
+#include "osc_kernels.h"
+
+namespace osc {
+namespace {
+
+constexpr int kMaxWarps = 32;
+
+template <int K>
+struct Tile {
+    double C[K];
+    Divisor md[K];
+    double Cn;   // spring of the first cell of the next thread
+    int lastj;   // index of the tile's last cell if this thread owns it, else -1
+    bool wall;   // this thread's cell 0 is the tile's first cell
+    int lane, warp, nwarps;
+};
+
+// acceleration_at for all K cells of this thread at positions p.
+template <int K>
+__device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], double (&a)[K],
+                                      double (*s_lo)[kMaxWarps], double (*s_hi)[kMaxWarps],
+                                      int &buf)
+{
+    double pl = __shfl_up_sync(kFull, p[K - 1], 1);
+    double pr = __shfl_down_sync(kFull, p[0], 1);
+    if (t.nwarps > 1) {
+        if (t.lane == 0)
+            s_lo[buf][t.warp] = p[0];
+        if (t.lane == 31)
+            s_hi[buf][t.warp] = p[K - 1];
+        __syncthreads();
+        if (t.lane == 0 && t.warp > 0)
+            pl = s_hi[buf][t.warp - 1];
+        if (t.lane == 31 && t.warp < t.nwarps - 1)
+            pr = s_lo[buf][t.warp + 1];
+        buf ^= 1;
+    }
+    double f[K];
+    f[0] = mul(t.C[0], t.wall ? p[0] : sub(p[0], pl));
+#pragma unroll
+    for (int j = 1; j < K; ++j)
+        f[j] = mul(t.C[j], sub(p[j], p[j - 1]));
+    const double fr = mul(t.Cn, sub(pr, p[K - 1]));
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const double fnext = (j + 1 < K) ? f[j + 1] : fr;
+        const double num = (j == t.lastj) ? -f[j] : sub(fnext, f[j]);
+        a[j] = div(num, t.md[j]);
+    }
+}
+
+// One classical RK4 step (oscillator.py:208-231) of the thread's K cells.
+template <int K>
+__device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&v)[K],
+                                     const StepConsts &k, double (*s_lo)[kMaxWarps],
+                                     double (*s_hi)[kMaxWarps], int &buf)
+{
+    double a[K], yp[K], yv[K], sx[K], sv[K];
+    accel<K>(t, x, a, s_lo, s_hi, buf);  // k1
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sx[j] = v[j];
+        sv[j] = a[j];
+        yp[j] = add(x[j], mul(k.half_dt, v[j]));
+        yv[j] = add(v[j], mul(k.half_dt, a[j]));
+    }
+    accel<K>(t, yp, a, s_lo, s_hi, buf);  // k2
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sx[j] = add(sx[j], mul(2.0, yv[j]));
+        sv[j] = add(sv[j], mul(2.0, a[j]));
+        yp[j] = add(x[j], mul(k.half_dt, yv[j]));
+        yv[j] = add(v[j], mul(k.half_dt, a[j]));
+    }
+    accel<K>(t, yp, a, s_lo, s_hi, buf);  // k3
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sx[j] = add(sx[j], mul(2.0, yv[j]));
+        sv[j] = add(sv[j], mul(2.0, a[j]));
+        yp[j] = add(x[j], mul(k.dt, yv[j]));
+        yv[j] = add(v[j], mul(k.dt, a[j]));
+    }
+    accel<K>(t, yp, a, s_lo, s_hi, buf);  // k4
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sx[j] = add(sx[j], yv[j]);
+        sv[j] = add(sv[j], a[j]);
+        x[j] = add(x[j], mul(k.dt6, sx[j]));
+        v[j] = add(v[j], mul(k.dt6, sv[j]));
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void load_state(const SegArgs &g, int64_t base, int64_t c0, int64_t cend,
+                                           double (&x)[K], double (&v)[K])
+{
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int64_t c = c0 + j;
+        x[j] = c < cend ? g.xin[base + c] : 0.0;
+        v[j] = c < cend ? g.vin[base + c] : 0.0;
+    }
+}
+
+template <int K>
+__device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v)[K], int64_t c0,
+                                          int64_t own_start, int64_t own_end)
+{
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int64_t c = c0 + j;
+        if (c >= own_start && c < own_end)
+            bad |= !(finite(x[j]) & finite(v[j]));
+    }
+    return bad;
+}
+
+// Register budget: K cells x ~10 live doubles per thread.
+template <int K>
+constexpr int max_threads() { return K <= 1 ? 1024 : K == 2 ? 512 : 256; }
+
+template <int K>
+__global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
+{
+    __shared__ double s_lo[2][kMaxWarps];
+    __shared__ double s_hi[2][kMaxWarps];
+
+    const int64_t buf_id = blockIdx.x / g.tiles;
+    const int64_t tile = blockIdx.x % g.tiles;
+    if (g.first_bad[buf_id] != 0)
+        return;  // already diverged: state is unspecified, as integrate raised
+
+    const int64_t TILE = static_cast<int64_t>(blockDim.x) * K;
+    const int64_t own_start = g.own_lo + tile * g.W;
+    const int64_t own_end = min(own_start + g.W, g.own_hi);
+    const int64_t L = max(static_cast<int64_t>(0), own_start - g.H);
+    const int64_t cend = min(L + TILE, g.n);  // one past the tile's last cell
+    const int64_t base = buf_id * g.n;
+    const int64_t c0 = L + static_cast<int64_t>(threadIdx.x) * K;
+
+    Tile<K> t;
+    t.lane = threadIdx.x & 31;
+    t.warp = threadIdx.x >> 5;
+    t.nwarps = blockDim.x >> 5;
+    t.wall = threadIdx.x == 0;
+    const int64_t last = cend - 1;
+    t.lastj = (last >= c0 && last < c0 + K) ? static_cast<int>(last - c0) : -1;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int64_t c = c0 + j;
+        t.C[j] = c < cend ? g.C[base + c] : 1.0;
+        t.md[j] = make_divisor(c < cend ? g.m[base + c] : 1.0);
+    }
+    t.Cn = (c0 + K < cend) ? g.C[base + c0 + K] : 1.0;
+
+    double x[K], v[K];
+    load_state<K>(g, base, c0, cend, x, v);
+    int buf = 0;
+    for (int64_t s = 0; s < g.nsteps; ++s)
+        step<K>(t, x, v, g.k, s_lo, s_hi, buf);
+
+    if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
+        // Divergence inside this launch: replay from the untouched input one
+        // step at a time to find the exact first bad step of the owned cells
+        // (NonFiniteStateError.step, oscillator.py:255-260).
+        load_state<K>(g, base, c0, cend, x, v);
+        for (int64_t s = 0; s < g.nsteps; ++s) {
+            step<K>(t, x, v, g.k, s_lo, s_hi, buf);
+            if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
+                if (threadIdx.x == 0)
+                    record_bad(&g.first_bad[buf_id], g.step0 + s + 1);
+                break;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int64_t c = c0 + j;
+        if (c >= own_start && c < own_end) {
+            g.xout[base + c] = x[j];
+            g.vout[base + c] = v[j];
+            if (g.xs) {
+                g.xs[base + c] = x[j];
+                g.vs[base + c] = v[j];
+            }
+        }
+    }
+}
+
+template <int K>
+cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
+{
+    if (threads > max_threads<K>() || threads % 32)
+        return cudaErrorInvalidConfiguration;
+    const int64_t blocks = g.tiles * g.nbuf;
+    chain_rk4_kernel<K><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(g);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream)
+{
+    switch (K) {
+    case 1: return launch_k<1>(g, threads, stream);
+    case 2: return launch_k<2>(g, threads, stream);
+    case 4: return launch_k<4>(g, threads, stream);
+    case 8: return launch_k<8>(g, threads, stream);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace osc

@@ -1,0 +1,182 @@
+// Off-loop operations of the drop-in API and the division self-test.
+//
+//   derivative  oscillator.py:184-191  (dvel = acceleration_at per cell)
+//   energy      oscillator.py:266-276  (sequential index-order sum, exact)
+#include "osc_device.cuh"
+#include "osc_kernels.h"
+
+namespace osc {
+namespace {
+
+// Cells of chain b are at x[b*chain_stride + i*cell_stride]: [B][s] uses
+// (s, 1); the batched 2-DOF SoA layout [2][B] uses (1, B).
+__global__ void derivative_kernel(const double *__restrict__ m, const double *__restrict__ C,
+                                  const double *__restrict__ x, double *__restrict__ dvel,
+                                  int64_t B, int64_t s, int64_t chain_stride,
+                                  int64_t cell_stride)
+{
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= B * s)
+        return;
+    const int64_t b = gid / s, i = gid % s;
+    const int64_t o = b * chain_stride;
+    const auto at = [&](const double *p, int64_t j) { return p[o + j * cell_stride]; };
+    // acceleration_at, oscillator.py:160-164, literally.
+    const double left = sub(at(x, i), i > 0 ? at(x, i - 1) : 0.0);
+    double a = mul(-at(C, i), left);
+    if (i + 1 < s)
+        a = add(a, mul(at(C, i + 1), sub(at(x, i + 1), at(x, i))));
+    dvel[o + i * cell_stride] = __ddiv_rn(a, at(m, i));
+}
+
+__global__ void energy_kernel(const double *__restrict__ m, const double *__restrict__ C,
+                              const double *__restrict__ x, const double *__restrict__ v,
+                              double *__restrict__ out, int64_t B, int64_t s,
+                              int64_t chain_stride, int64_t cell_stride)
+{
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= B)
+        return;
+    const int64_t o = b * chain_stride;
+    double total = 0.0;
+    double prev = 0.0;
+    for (int64_t i = 0; i < s; ++i) {
+        const int64_t c = o + i * cell_stride;
+        const double vi = v[c], xi = x[c];
+        total = add(total, mul(mul(mul(0.5, m[c]), vi), vi));
+        const double ext = sub(xi, prev);  // pos[i] - (pos[i-1] if i > 0 else 0.0)
+        total = add(total, mul(mul(mul(0.5, C[c]), ext), ext));
+        prev = xi;
+    }
+    out[b] = total;
+}
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t z)
+{
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// Compare div(a, make_divisor(b)) with __ddiv_rn(a, b) bit for bit.
+//   mode 0: b in [0.5, 2) (the configs' masses), a any bit pattern
+//   mode 1: b any positive finite double (normal or subnormal), a any pattern
+//   mode 2: b in [0.5, 2), |a| in [2^-40, 2^40) (physical accelerations)
+__global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
+                                      unsigned long long *mismatches)
+{
+    unsigned long long bad = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r1 = splitmix(seed ^ (2 * static_cast<uint64_t>(i)));
+        const uint64_t r2 = splitmix(seed ^ (2 * static_cast<uint64_t>(i) + 1));
+        const uint64_t mant_b = r2 & 0x000fffffffffffffull;
+        uint64_t bb;
+        if (mode == 1) {
+            uint64_t e = (r2 >> 52) & 0x7ff;
+            if (e == 0x7ff)
+                e = 0x7fe;
+            bb = (e << 52) | mant_b;  // includes subnormals, never zero below
+            if (bb == 0)
+                bb = 1;
+        } else {
+            bb = ((r2 >> 63) ? 0x3fe0000000000000ull : 0x3ff0000000000000ull) | mant_b;
+        }
+        uint64_t ab = r1;
+        if (mode == 2) {
+            const uint64_t e = 1023 - 40 + ((r1 >> 52) % 80);
+            ab = (r1 & 0x800fffffffffffffull) | (e << 52);
+        } else if ((r1 & 0xff) == 0) {
+            ab = r1 & 0x8000000000000000ull;  // inject signed zeros
+        }
+        const double a = __longlong_as_double(static_cast<long long>(ab));
+        const double b = __longlong_as_double(static_cast<long long>(bb));
+        const double got = div(a, make_divisor(b));
+        const double want = __ddiv_rn(a, b);
+        const bool both_nan = (got != got) && (want != want);
+        if (!both_nan && __double_as_longlong(got) != __double_as_longlong(want))
+            ++bad;
+    }
+    if (bad)
+        atomicAdd(mismatches, bad);
+}
+
+// FP64 issue-rate microbenchmark: 8 independent DFMA (mode 0) or DADD
+// (mode 1) chains per thread.  Gives the measured DP-pipe peak the compute
+// roofline of K1/K2 is quoted against (MEASURED_PEAKS.json has no FP64).
+__global__ void fp64_peak_kernel(int64_t iters, int mode, double *sink)
+{
+    double a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        a[j] = 1.0 + 1e-3 * (threadIdx.x + j);
+    const double b = 0.999999, c = 1e-7;
+    if (mode == 0) {
+        for (int64_t i = 0; i < iters; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                a[j] = __fma_rn(a[j], b, c);
+    } else {
+        for (int64_t i = 0; i < iters; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                a[j] = __dadd_rn(a[j], c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        s += a[j];
+    if (s == 12345.678)
+        sink[threadIdx.x] = s;
+}
+
+}  // namespace
+
+cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lanes_ops,
+                             cudaStream_t stream)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 4, threads = 512;
+    fp64_peak_kernel<<<blocks, threads, 0, stream>>>(iters, mode, sink);
+    *lanes_ops = int64_t(blocks) * threads * iters * 8;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_derivative(const double *m, const double *C, const double *x, double *dvel,
+                              int64_t B, int64_t s, bool cell_major, cudaStream_t stream)
+{
+    const int64_t total = B * s;
+    if (total == 0)
+        return cudaSuccess;
+    const int threads = 256;
+    derivative_kernel<<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0,
+                        stream>>>(m, C, x, dvel, B, s, cell_major ? 1 : s, cell_major ? B : 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy(const double *m, const double *C, const double *x, const double *v,
+                          double *out, int64_t B, int64_t s, bool cell_major,
+                          cudaStream_t stream)
+{
+    if (B == 0)
+        return cudaSuccess;
+    const int threads = 128;
+    energy_kernel<<<static_cast<unsigned>((B + threads - 1) / threads), threads, 0, stream>>>(
+        m, C, x, v, out, B, s, cell_major ? 1 : s, cell_major ? B : 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_division(int64_t n, uint64_t seed, int mode,
+                                  unsigned long long *mismatches, cudaStream_t stream)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    check_division_kernel<<<sms * 8, 256, 0, stream>>>(n, seed, mode, mismatches);
+    return cudaGetLastError();
+}
+
+}  // namespace osc

@@ -1,0 +1,46 @@
+// Internal launch interface between the C-ABI layer (capi.cu) and kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "osc_device.cuh"
+
+namespace osc {
+
+// One launch of the chain kernel over nbuf buffers of n cells each.
+struct SegArgs {
+    const double *m, *C;     // [nbuf][n]
+    const double *xin, *vin; // [nbuf][n] state at step0
+    double *xout, *vout;     // [nbuf][n] owned cells written after nsteps
+    double *xs, *vs;         // optional copy of the owned cells (a sample slot)
+    int64_t *first_bad;      // [nbuf], 0 = finite so far
+    int64_t n, nbuf;
+    int64_t own_lo, own_hi;  // owned cell range of every buffer
+    int64_t W, H;            // owned cells per tile, halo cells per side
+    int64_t tiles;           // tiles per buffer
+    StepConsts k;
+    int64_t nsteps, step0;
+};
+
+cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
+                          StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                          int64_t *first_bad, cudaStream_t stream);
+
+cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream);
+
+// cell_major: [s][B] layout (the batched 2-DOF SoA); else [B][s].
+cudaError_t launch_derivative(const double *m, const double *C, const double *x, double *dvel,
+                              int64_t B, int64_t s, bool cell_major, cudaStream_t stream);
+
+cudaError_t launch_energy(const double *m, const double *C, const double *x, const double *v,
+                          double *out, int64_t B, int64_t s, bool cell_major,
+                          cudaStream_t stream);
+
+cudaError_t launch_check_division(int64_t n, uint64_t seed, int mode,
+                                  unsigned long long *mismatches, cudaStream_t stream);
+
+cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lanes_ops,
+                             cudaStream_t stream);
+
+}  // namespace osc

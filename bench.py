@@ -38,9 +38,10 @@ METRIC = "DOF-steps/s"
 UNIT = "DOF-steps/s"
 HBM_BYTES_PER_DOF_STEP = 48  # read x,v,m,C + write x,v, one step per round trip
 FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42}
-# DP-pipe instructions per DOF-step in the kernels (SASS-derived):
-# batch2: 68 +,-,* and 8 divisions x 3 (hoisted reciprocal) per system-step.
-DP_INST_PER_DOF_STEP = {"C1": 46, "C2": 46, "C3": 52, "C4": 52}
+# DP-pipe instructions per DOF-step in the hot loops, counted in SASS with
+# scripts/sass_stats.py --loop: batch2 96 per system-step; chain
+# 412 per 8 cells (K=8, the default shape of both chain modes) per step.
+DP_INST_PER_DOF_STEP = {"C1": 48, "C2": 48, "C3": 51.5, "C4": 51.5}
 
 
 def peaks():
@@ -139,13 +140,13 @@ class Workload:
                          "systems_per_gpu": workloads.C2_B}
         elif name == "C4":
             arrays = workloads.c4(rank=rank)
-            self.kernel = "chain_rk4_kernel<4>"
+            self.kernel = "chain_rk4_kernel<8>"
             self.launches = -(-p.nsteps // 512)
             self.desc = {"workload": "C4: 4096 chains x 1024 cells, [B][s]",
                          "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
         elif name == "C3":
             arrays = workloads.c3()
-            T = halo or 32
+            T = halo or 16
             self.kernel = "chain_rk4_kernel<8>"
             self.launches = -(-p.nsteps // T)
             self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -59,23 +60,41 @@ osc::StepConsts consts(double dt)
 
 constexpr int64_t kWholeChainMax = 2048;  // 256 threads x 8 cells
 constexpr int64_t kWholeChainSteps = 512; // steps per launch in whole-chain mode
-constexpr int kTileK = 8, kTileThreads = 256;
+// Tiled shape, measured on B200 for s = 2^24 (profiles/r01): 8 cells x 128
+// threads with 16-step halos beat 8x256 (T=16,32,64) and 4x256.
+constexpr int kTileK = 8, kTileThreads = 128;
 constexpr int64_t kTile = int64_t(kTileK) * kTileThreads;
-constexpr int64_t kDefaultHaloSteps = 32;
+constexpr int64_t kDefaultHaloSteps = 16;
 
 void pick_whole(int64_t s, int &K, int &threads)
 {
-    // Fewest cells per thread that keep the CTA at <= 256 threads (the
-    // kernel's register budget allows 256 threads up to K = 8).
+    // Fewest cells per thread that keep the CTA at <= 128 threads, else 256
+    // threads of 8 cells.  Measured on B200 for s = 1024 (profiles/r01):
+    // K=8 x 128 threads 2.81e11 DOF-steps/s, K=4 x 256 2.61e11, K=2 x 512 1.19e11.
     K = 8;
     for (int k : {1, 2, 4, 8}) {
-        if ((s + k - 1) / k <= 256) {
+        if ((s + k - 1) / k <= 128) {
             K = k;
             break;
         }
     }
     const int64_t t = (s + K - 1) / K;
     threads = static_cast<int>(((t + 31) / 32) * 32);
+}
+
+// Tuning hook (benchmarks only): OSC_TILE="K,threads" / OSC_WHOLE="K,threads"
+// override the tiled / whole-chain launch shapes.  Read-only process state.
+bool env_shape(const char *name, int &K, int &threads)
+{
+    const char *e = std::getenv(name);
+    int k = 0, t = 0;
+    if (!e || std::sscanf(e, "%d,%d", &k, &t) != 2)
+        return false;
+    if ((k != 1 && k != 2 && k != 4 && k != 8) || t < 32 || t > 1024 || t % 32)
+        return false;
+    K = k;
+    threads = t;
+    return true;
 }
 
 struct Scratch {
@@ -141,19 +160,26 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     g.k = consts(dt);
     int K = kTileK, threads = kTileThreads;
     int64_t per_launch;
-    if (s <= kWholeChainMax) {
+    int wk = 0, wt = 0;
+    const bool whole_env = env_shape("OSC_WHOLE", wk, wt) && int64_t(wk) * wt >= s;
+    if (s <= kWholeChainMax || whole_env) {
         pick_whole(s, K, threads);
+        if (whole_env) {
+            K = wk;
+            threads = wt;
+        }
         g.W = s;
         g.H = 0;
         g.tiles = 1;
         per_launch = kWholeChainSteps;
     } else {
         const int64_t T = halo_steps > 0 ? halo_steps : kDefaultHaloSteps;
+        env_shape("OSC_TILE", K, threads);
         g.H = 2 * T;
-        g.W = kTile - 2 * g.H;
+        g.W = int64_t(K) * threads - 2 * g.H;
         if (g.W < 1)
             return fail(OSC_INVALID, "halo_steps=%lld too deep for a %lld-cell tile",
-                        (long long)T, (long long)kTile);
+                        (long long)T, (long long)K * threads);
         g.tiles = (s + g.W - 1) / g.W;
         per_launch = T;
     }

@@ -21,33 +21,35 @@ struct Sys2 {
     double x0, x1, v0, v1;
 };
 
+template <bool kExact>
 __device__ __forceinline__ void accel2(double p0, double p1, double C0, double C1,
                                        const Divisor &m0, const Divisor &m1, double &a0,
-                                       double &a1)
+                                       double &a1, bool &ok)
 {
     const double d1 = sub(p1, p0);
     const double f1 = mul(C1, d1);
     const double g0 = mul(-C0, p0);
-    a0 = div(add(g0, f1), m0);
-    a1 = div(-f1, m1);
+    a0 = qdiv<kExact>(add(g0, f1), m0, ok);
+    a1 = qdiv<kExact>(-f1, m1, ok);
 }
 
 // One classical RK4 step (oscillator.py:208-231).  The combination sums are
 // accumulated left to right exactly as combine_value's
 // ((k1 + 2k2) + 2k3) + k4; 2.0*k is exact.
+template <bool kExact>
 __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divisor &m0,
-                                      const Divisor &m1, const StepConsts &k)
+                                      const Divisor &m1, const StepConsts &k, bool &ok)
 {
     double a0, a1;
     // k1 at the step start; position slopes are the velocities.
-    accel2(s.x0, s.x1, C0, C1, m0, m1, a0, a1);
+    accel2<kExact>(s.x0, s.x1, C0, C1, m0, m1, a0, a1, ok);
     double sx0 = s.v0, sx1 = s.v1, sv0 = a0, sv1 = a1;
     double yv0 = add(s.v0, mul(k.half_dt, a0));
     double yv1 = add(s.v1, mul(k.half_dt, a1));
     double yp0 = add(s.x0, mul(k.half_dt, s.v0));
     double yp1 = add(s.x1, mul(k.half_dt, s.v1));
     // k2 at the midpoint; y2v doubles as the k2 position slope.
-    accel2(yp0, yp1, C0, C1, m0, m1, a0, a1);
+    accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
     sx0 = add(sx0, mul(2.0, yv0));
     sx1 = add(sx1, mul(2.0, yv1));
     sv0 = add(sv0, mul(2.0, a0));
@@ -57,7 +59,7 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     yv0 = add(s.v0, mul(k.half_dt, a0));
     yv1 = add(s.v1, mul(k.half_dt, a1));
     // k3 at the refined midpoint.
-    accel2(yp0, yp1, C0, C1, m0, m1, a0, a1);
+    accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
     sx0 = add(sx0, mul(2.0, yv0));
     sx1 = add(sx1, mul(2.0, yv1));
     sv0 = add(sv0, mul(2.0, a0));
@@ -67,7 +69,7 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     yv0 = add(s.v0, mul(k.dt, a0));
     yv1 = add(s.v1, mul(k.dt, a1));
     // k4 at the endpoint, then the weighted combination.
-    accel2(yp0, yp1, C0, C1, m0, m1, a0, a1);
+    accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
     sx0 = add(sx0, yv0);
     sx1 = add(sx1, yv1);
     sv0 = add(sv0, a0);
@@ -103,6 +105,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         vs[i] = s.v0;
         vs[B + i] = s.v1;
     }
+    const bool ok0 = divisor_fast_ok(m0) & divisor_fast_ok(m1);
     int64_t bad = 0;
     int64_t kstep = 0;
     while (kstep < nsteps) {
@@ -113,21 +116,25 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         if (n > kChunk)
             n = kChunk;
         const Sys2 saved = s;
+        bool ok = ok0;
         for (int j = 0; j < n; ++j)
-            step2(s, C0, C1, m0, m1, k);
-        if (!finite2(s)) {
-            // Non-finite values are absorbing under + - * /, so replaying the
-            // chunk one step at a time finds the exact first bad step
-            // (integrate's NonFiniteStateError.step, oscillator.py:255-260).
+            step2<false>(s, C0, C1, m0, m1, k, ok);
+        if (!(ok & finite2(s))) {
+            // A division left nvcc's fast path or a value went non-finite:
+            // replay the chunk with IEEE division, checking every step.
+            // Non-finite values are absorbing under + - * /, so the first
+            // non-finite step is integrate's NonFiniteStateError.step
+            // (oscillator.py:255-260).
             s = saved;
             for (int j = 0; j < n; ++j) {
-                step2(s, C0, C1, m0, m1, k);
+                step2<true>(s, C0, C1, m0, m1, k, ok);
                 if (!finite2(s)) {
                     bad = kstep + j + 1;
                     break;
                 }
             }
-            break;
+            if (bad)
+                break;
         }
         kstep += n;
         if (xs && kstep % stride == 0) {

@@ -36,17 +36,22 @@ template <int K>
 struct Tile {
     double C[K];
     Divisor md[K];
-    double Cn;   // spring of the first cell of the next thread
-    int lastj;   // index of the tile's last cell if this thread owns it, else -1
-    bool wall;   // this thread's cell 0 is the tile's first cell
+    double Cn;     // spring of the first cell of the next thread
+    int lastj;     // index of the tile's last cell if this thread owns it, else -1
+    int validn;    // cells of this thread inside the tile (pad variant)
+    bool first;    // this thread's cell 0 is the tile's first cell (wall side)
+    bool last;     // this thread's cell K-1 is the tile's last cell (free side)
     int lane, warp, nwarps;
 };
 
-// acceleration_at for all K cells of this thread at positions p.
-template <int K>
+// acceleration_at for the K cells of this thread at positions p.  kPad: the
+// tile extends past the buffer end, so cells >= validn are padding whose
+// numerators are replaced by 1.0 (they never feed a real cell: the last real
+// cell has no right neighbour) to keep them off the slow division path.
+template <int K, bool kPad, bool kExact>
 __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], double (&a)[K],
                                       double (*s_lo)[kMaxWarps], double (*s_hi)[kMaxWarps],
-                                      int &buf)
+                                      int &buf, bool &ok)
 {
     double pl = __shfl_up_sync(kFull, p[K - 1], 1);
     double pr = __shfl_down_sync(kFull, p[0], 1);
@@ -63,27 +68,35 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
         buf ^= 1;
     }
     double f[K];
-    f[0] = mul(t.C[0], t.wall ? p[0] : sub(p[0], pl));
+    f[0] = mul(t.C[0], t.first ? p[0] : sub(p[0], pl));  // d_0 = x_0 - 0.0 == x_0
 #pragma unroll
     for (int j = 1; j < K; ++j)
         f[j] = mul(t.C[j], sub(p[j], p[j - 1]));
     const double fr = mul(t.Cn, sub(pr, p[K - 1]));
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        const double fnext = (j + 1 < K) ? f[j + 1] : fr;
-        const double num = (j == t.lastj) ? -f[j] : sub(fnext, f[j]);
-        a[j] = div(num, t.md[j]);
+        double num;
+        if constexpr (kPad) {
+            const double fnext = (j + 1 < K) ? f[j + 1] : fr;
+            num = (j == t.lastj) ? -f[j] : sub(fnext, f[j]);
+            num = (j < t.validn) ? num : 1.0;
+        } else if (j + 1 < K) {
+            num = sub(f[j + 1], f[j]);
+        } else {
+            num = t.last ? -f[j] : sub(fr, f[j]);
+        }
+        a[j] = qdiv<kExact>(num, t.md[j], ok);
     }
 }
 
 // One classical RK4 step (oscillator.py:208-231) of the thread's K cells.
-template <int K>
+template <int K, bool kPad, bool kExact>
 __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&v)[K],
                                      const StepConsts &k, double (*s_lo)[kMaxWarps],
-                                     double (*s_hi)[kMaxWarps], int &buf)
+                                     double (*s_hi)[kMaxWarps], int &buf, bool &ok)
 {
     double a[K], yp[K], yv[K], sx[K], sv[K];
-    accel<K>(t, x, a, s_lo, s_hi, buf);  // k1
+    accel<K, kPad, kExact>(t, x, a, s_lo, s_hi, buf, ok);  // k1
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = v[j];
@@ -91,7 +104,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
         yp[j] = add(x[j], mul(k.half_dt, v[j]));
         yv[j] = add(v[j], mul(k.half_dt, a[j]));
     }
-    accel<K>(t, yp, a, s_lo, s_hi, buf);  // k2
+    accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k2
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], mul(2.0, yv[j]));
@@ -99,7 +112,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
         yp[j] = add(x[j], mul(k.half_dt, yv[j]));
         yv[j] = add(v[j], mul(k.half_dt, a[j]));
     }
-    accel<K>(t, yp, a, s_lo, s_hi, buf);  // k3
+    accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k3
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], mul(2.0, yv[j]));
@@ -107,7 +120,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
         yp[j] = add(x[j], mul(k.dt, yv[j]));
         yv[j] = add(v[j], mul(k.dt, a[j]));
     }
-    accel<K>(t, yp, a, s_lo, s_hi, buf);  // k4
+    accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k4
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], yv[j]);
@@ -118,8 +131,8 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
 }
 
 template <int K>
-__device__ __forceinline__ void load_state(const SegArgs &g, int64_t base, int64_t c0, int64_t cend,
-                                           double (&x)[K], double (&v)[K])
+__device__ __forceinline__ void load_state(const SegArgs &g, int64_t base, int64_t c0,
+                                           int64_t cend, double (&x)[K], double (&v)[K])
 {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -147,7 +160,7 @@ __device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v
 template <int K>
 constexpr int max_threads() { return K <= 1 ? 1024 : K == 2 ? 512 : 256; }
 
-template <int K>
+template <int K, bool kPad>
 __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 {
     __shared__ double s_lo[2][kMaxWarps];
@@ -161,7 +174,9 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
     const int64_t TILE = static_cast<int64_t>(blockDim.x) * K;
     const int64_t own_start = g.own_lo + tile * g.W;
     const int64_t own_end = min(own_start + g.W, g.own_hi);
-    const int64_t L = max(static_cast<int64_t>(0), own_start - g.H);
+    int64_t L = max(static_cast<int64_t>(0), own_start - g.H);
+    if (!kPad && L + TILE > g.n)
+        L = g.n - TILE;  // slide the last tile left so it ends at the buffer end: no padding
     const int64_t cend = min(L + TILE, g.n);  // one past the tile's last cell
     const int64_t base = buf_id * g.n;
     const int64_t c0 = L + static_cast<int64_t>(threadIdx.x) * K;
@@ -170,30 +185,38 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
     t.lane = threadIdx.x & 31;
     t.warp = threadIdx.x >> 5;
     t.nwarps = blockDim.x >> 5;
-    t.wall = threadIdx.x == 0;
-    const int64_t last = cend - 1;
-    t.lastj = (last >= c0 && last < c0 + K) ? static_cast<int>(last - c0) : -1;
+    t.first = threadIdx.x == 0;
+    t.last = threadIdx.x == blockDim.x - 1;
+    const int64_t lastc = cend - 1;
+    t.lastj = (lastc >= c0 && lastc < c0 + K) ? static_cast<int>(lastc - c0) : -1;
+    t.validn = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(K),
+                                                                 cend - c0)));
+    bool ok0 = true;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int64_t c = c0 + j;
         t.C[j] = c < cend ? g.C[base + c] : 1.0;
         t.md[j] = make_divisor(c < cend ? g.m[base + c] : 1.0);
+        ok0 &= divisor_fast_ok(t.md[j]);
     }
     t.Cn = (c0 + K < cend) ? g.C[base + c0 + K] : 1.0;
 
     double x[K], v[K];
     load_state<K>(g, base, c0, cend, x, v);
     int buf = 0;
+    bool ok = ok0;
     for (int64_t s = 0; s < g.nsteps; ++s)
-        step<K>(t, x, v, g.k, s_lo, s_hi, buf);
+        step<K, kPad, false>(t, x, v, g.k, s_lo, s_hi, buf, ok);
 
-    if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
-        // Divergence inside this launch: replay from the untouched input one
-        // step at a time to find the exact first bad step of the owned cells
-        // (NonFiniteStateError.step, oscillator.py:255-260).
+    if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, own_start, own_end))) {
+        // A division left nvcc's fast path, or a value went non-finite:
+        // replay the launch from the untouched input with IEEE division,
+        // checking every step, to keep exact values and find the exact first
+        // bad step of the owned cells (NonFiniteStateError.step,
+        // oscillator.py:255-260).
         load_state<K>(g, base, c0, cend, x, v);
         for (int64_t s = 0; s < g.nsteps; ++s) {
-            step<K>(t, x, v, g.k, s_lo, s_hi, buf);
+            step<K, kPad, true>(t, x, v, g.k, s_lo, s_hi, buf, ok);
             if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
                 if (threadIdx.x == 0)
                     record_bad(&g.first_bad[buf_id], g.step0 + s + 1);
@@ -221,7 +244,12 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
     if (threads > max_threads<K>() || threads % 32)
         return cudaErrorInvalidConfiguration;
     const int64_t blocks = g.tiles * g.nbuf;
-    chain_rk4_kernel<K><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(g);
+    const int64_t TILE = int64_t(threads) * K;
+    // Padding is needed only when a tile is longer than the whole buffer.
+    if (TILE > g.n)
+        chain_rk4_kernel<K, true><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(g);
+    else
+        chain_rk4_kernel<K, false><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(g);
     return cudaGetLastError();
 }
 

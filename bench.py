@@ -39,9 +39,9 @@ UNIT = "DOF-steps/s"
 HBM_BYTES_PER_DOF_STEP = 48  # read x,v,m,C + write x,v, one step per round trip
 FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42}
 # DP-pipe instructions per DOF-step in the hot loops, counted in SASS with
-# scripts/sass_stats.py --loop: batch2 96 per system-step; chain
-# 412 per 8 cells (K=8, the default shape of both chain modes) per step.
-DP_INST_PER_DOF_STEP = {"C1": 48, "C2": 48, "C3": 51.5, "C4": 51.5}
+# scripts/sass_stats.py --loop: batch2 184 per 2 systems per step
+# (NS=2); chain 396 per 8 cells (K=8, the default shape of both chain modes).
+DP_INST_PER_DOF_STEP = {"C1": 46, "C2": 46, "C3": 49.5, "C4": 49.5}
 
 
 def peaks():

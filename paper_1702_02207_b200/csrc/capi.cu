@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 
 #include "../../include/osc_b200.h"
 #include "osc_kernels.h"
@@ -95,6 +96,23 @@ bool env_shape(const char *name, int &K, int &threads)
     K = k;
     threads = t;
     return true;
+}
+
+// Keep freed stream-ordered allocations in the device's default pool instead
+// of returning them to the driver at every synchronisation (the default
+// release threshold is 0), so repeated host-API calls do not re-map memory.
+void retain_pool_memory()
+{
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev)
+        return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
 }
 
 struct Scratch {
@@ -189,6 +207,7 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
         OSC_CUDA(cudaMemcpyAsync(xs, x, bytes, cudaMemcpyDeviceToDevice, stream));
         OSC_CUDA(cudaMemcpyAsync(vs, v, bytes, cudaMemcpyDeviceToDevice, stream));
     }
+    retain_pool_memory();
     Scratch scratch;
     scratch.s = stream;
     OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch.p), 2 * bytes, stream));
@@ -313,15 +332,11 @@ int osc_bench_fp64(int64_t iters, int mode, double *sink, int64_t *lane_ops, voi
 
 namespace {
 
-struct DevBuf {
-    void *p = nullptr;
-    ~DevBuf()
-    {
-        if (p)
-            cudaFree(p);
-    }
-};
-
+// Host-pointer form of a batched run.  The batch is cut into chunks that are
+// pipelined over a few streams: chunk c's H2D copy, kernels and D2H copy are
+// ordered on stream c % S, so copies of one chunk overlap the compute of
+// another and consecutive chunks' kernels fill each other's tail waves.
+// Sampled runs use a single chunk (their [nsamp][...] layout spans the batch).
 int host_run(bool chains, const double *m, const double *C, double *x, double *v, int64_t B,
              int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
              int64_t *first_bad)
@@ -334,35 +349,95 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         return OSC_OK;
     if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
-    cudaStream_t st = cudaStreamPerThread;
+    retain_pool_memory();
     const size_t cells = static_cast<size_t>(B * s);
     const size_t bytes = cells * sizeof(double);
     const size_t nsamp = xs ? static_cast<size_t>(1 + nsteps / stride) : 0;
-    DevBuf buf;
+
+    // chunking: >= 8 MB of state per chunk, at most 8 chunks
+    int64_t nchunk = 1;
+    if (!xs && B > 1)
+        nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 23)}));
+    const int nstream = static_cast<int>(std::min<int64_t>(nchunk, 3));
+    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+    for (int i = 0; i < nstream; ++i)
+        OSC_CUDA(cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking));
+    struct Cleanup {
+        cudaStream_t *st;
+        int n;
+        void *mem = nullptr;
+        ~Cleanup()
+        {
+            for (int i = 0; i < n; ++i)
+                cudaStreamSynchronize(st[i]);  // every stream is done with mem
+            if (mem)
+                cudaFreeAsync(mem, st[0]);
+            for (int i = 0; i < n; ++i) {
+                cudaStreamSynchronize(st[i]);
+                cudaStreamDestroy(st[i]);
+            }
+        }
+    } cleanup{streams, nstream};
+
     const size_t total = 4 * bytes + B * sizeof(int64_t) + 2 * nsamp * bytes;
-    OSC_CUDA(cudaMalloc(&buf.p, total));
-    double *dm = static_cast<double *>(buf.p), *dC = dm + cells, *dx = dC + cells,
+    OSC_CUDA(cudaMallocAsync(&cleanup.mem, total, streams[0]));
+    cudaEvent_t ready;
+    OSC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    OSC_CUDA(cudaEventRecord(ready, streams[0]));
+    for (int i = 1; i < nstream; ++i)
+        OSC_CUDA(cudaStreamWaitEvent(streams[i], ready, 0));
+    cudaEventDestroy(ready);
+
+    double *dm = static_cast<double *>(cleanup.mem), *dC = dm + cells, *dx = dC + cells,
            *dv = dx + cells;
     int64_t *dfb = reinterpret_cast<int64_t *>(dv + cells);
     double *dxs = xs ? reinterpret_cast<double *>(dfb + B) : nullptr;
     double *dvs = xs ? dxs + nsamp * cells : nullptr;
-    OSC_CUDA(cudaMemcpyAsync(dm, m, bytes, cudaMemcpyHostToDevice, st));
-    OSC_CUDA(cudaMemcpyAsync(dC, C, bytes, cudaMemcpyHostToDevice, st));
-    OSC_CUDA(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, st));
-    OSC_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, st));
-    int rc = chains ? osc_rk4_chains(dm, dC, dx, dv, B, s, dt, nsteps, stride, dxs, dvs, dfb, 0,
-                                     st)
-                    : osc_rk4_batch2(dm, dC, dx, dv, B, dt, nsteps, stride, dxs, dvs, dfb, st);
-    if (rc != OSC_OK)
-        return rc;
-    OSC_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, st));
-    OSC_CUDA(cudaMemcpyAsync(v, dv, bytes, cudaMemcpyDeviceToHost, st));
-    OSC_CUDA(cudaMemcpyAsync(first_bad, dfb, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (xs) {
-        OSC_CUDA(cudaMemcpyAsync(xs, dxs, nsamp * bytes, cudaMemcpyDeviceToHost, st));
-        OSC_CUDA(cudaMemcpyAsync(vs, dvs, nsamp * bytes, cudaMemcpyDeviceToHost, st));
+    const auto H2D = cudaMemcpyHostToDevice;
+    const auto D2H = cudaMemcpyDeviceToHost;
+
+    for (int64_t c = 0; c < nchunk; ++c) {
+        cudaStream_t st = streams[c % nstream];
+        const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
+        int rc;
+        if (chains) {
+            // [B][s]: a chunk of chains is one contiguous block per array
+            const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
+            OSC_CUDA(cudaMemcpyAsync(dm + o, m + o, n, H2D, st));
+            OSC_CUDA(cudaMemcpyAsync(dC + o, C + o, n, H2D, st));
+            OSC_CUDA(cudaMemcpyAsync(dx + o, x + o, n, H2D, st));
+            OSC_CUDA(cudaMemcpyAsync(dv + o, v + o, n, H2D, st));
+            rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps, stride, dxs,
+                                dvs, dfb + b0, 0, st);
+            if (rc != OSC_OK)
+                return rc;
+            OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));
+            OSC_CUDA(cudaMemcpyAsync(v + o, dv + o, n, D2H, st));
+        } else {
+            // [2][B]: the chunk is packed as its own [2][nb] block on the device
+            const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
+            const double *hs[4] = {m, C, x, v};
+            double *ds[4] = {dm, dC, dx, dv};
+            for (int a = 0; a < 4; ++a)
+                for (int r = 0; r < 2; ++r)
+                    OSC_CUDA(cudaMemcpyAsync(ds[a] + o + r * nb, hs[a] + r * B + b0, n, H2D, st));
+            rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride, dxs, dvs,
+                                dfb + b0, st);
+            if (rc != OSC_OK)
+                return rc;
+            for (int r = 0; r < 2; ++r) {
+                OSC_CUDA(cudaMemcpyAsync(x + r * B + b0, dx + o + r * nb, n, D2H, st));
+                OSC_CUDA(cudaMemcpyAsync(v + r * B + b0, dv + o + r * nb, n, D2H, st));
+            }
+        }
+        OSC_CUDA(cudaMemcpyAsync(first_bad + b0, dfb + b0, nb * sizeof(int64_t), D2H, st));
     }
-    OSC_CUDA(cudaStreamSynchronize(st));
+    if (xs) {
+        OSC_CUDA(cudaMemcpyAsync(xs, dxs, nsamp * bytes, D2H, streams[0]));
+        OSC_CUDA(cudaMemcpyAsync(vs, dvs, nsamp * bytes, D2H, streams[0]));
+    }
+    for (int i = 0; i < nstream; ++i)
+        OSC_CUDA(cudaStreamSynchronize(streams[i]));
     int64_t worst = -1;
     for (int64_t b = 0; b < B; ++b)
         if (first_bad[b] != 0 && (worst < 0 || first_bad[b] < first_bad[worst]))

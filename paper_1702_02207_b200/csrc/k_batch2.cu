@@ -14,8 +14,14 @@
 #include "osc_device.cuh"
 #include "osc_kernels.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace osc {
 namespace {
+
+// Default launch shape (profiles/r01 sweep).
+constexpr int kBatch2NS = 2, kBatch2Threads = 128;
 
 struct Sys2 {
     double x0, x1, v0, v1;
@@ -52,8 +58,8 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
     sx0 = add(sx0, mul(2.0, yv0));
     sx1 = add(sx1, mul(2.0, yv1));
-    sv0 = add(sv0, mul(2.0, a0));
-    sv1 = add(sv1, mul(2.0, a1));
+    sv0 = add_twice<kExact>(sv0, a0);
+    sv1 = add_twice<kExact>(sv1, a1);
     yp0 = add(s.x0, mul(k.half_dt, yv0));
     yp1 = add(s.x1, mul(k.half_dt, yv1));
     yv0 = add(s.v0, mul(k.half_dt, a0));
@@ -62,8 +68,8 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
     sx0 = add(sx0, mul(2.0, yv0));
     sx1 = add(sx1, mul(2.0, yv1));
-    sv0 = add(sv0, mul(2.0, a0));
-    sv1 = add(sv1, mul(2.0, a1));
+    sv0 = add_twice<kExact>(sv0, a0);
+    sv1 = add_twice<kExact>(sv1, a1);
     yp0 = add(s.x0, mul(k.dt, yv0));
     yp1 = add(s.x1, mul(k.dt, yv1));
     yv0 = add(s.v0, mul(k.dt, a0));
@@ -87,26 +93,48 @@ __device__ __forceinline__ bool finite2(const Sys2 &s)
 
 constexpr int kChunk = 64;  // steps between divergence checks
 
+// NS systems per thread, interleaved for instruction-level parallelism:
+// system j of thread t in block b is b*NS*blockDim + j*blockDim + t, so each
+// load/store of a warp stays one contiguous 256 B run.  Indices past B
+// duplicate the last system and are never stored.
+template <int NS>
 __global__ void __launch_bounds__(256)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
                   StepConsts k, int64_t nsteps, int64_t stride, double *__restrict__ xs,
                   double *__restrict__ vs, int64_t *__restrict__ first_bad)
 {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= B)
-        return;
-    const Divisor m0 = make_divisor(m[i]), m1 = make_divisor(m[B + i]);
-    const double C0 = C[i], C1 = C[B + i];
-    Sys2 s{x[i], x[B + i], v[i], v[B + i]};
-    if (xs) {
-        xs[i] = s.x0;
-        xs[B + i] = s.x1;
-        vs[i] = s.v0;
-        vs[B + i] = s.v1;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * NS + threadIdx.x;
+    int64_t idx[NS];
+    bool live[NS];
+    Divisor m0[NS], m1[NS];
+    double C0[NS], C1[NS];
+    Sys2 s[NS];
+    bool ok0 = true;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        const int64_t gi = base + static_cast<int64_t>(j) * blockDim.x;
+        live[j] = gi < B;
+        idx[j] = live[j] ? gi : B - 1;
+        const int64_t i = idx[j];
+        m0[j] = make_divisor(m[i]);
+        m1[j] = make_divisor(m[B + i]);
+        C0[j] = C[i];
+        C1[j] = C[B + i];
+        s[j] = Sys2{x[i], x[B + i], v[i], v[B + i]};
+        ok0 &= divisor_fast_ok(m0[j]) & divisor_fast_ok(m1[j]);
+        if (xs && live[j]) {
+            xs[i] = s[j].x0;
+            xs[B + i] = s[j].x1;
+            vs[i] = s[j].v0;
+            vs[B + i] = s[j].v1;
+        }
     }
-    const bool ok0 = divisor_fast_ok(m0) & divisor_fast_ok(m1);
-    int64_t bad = 0;
+    int64_t bad[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+        bad[j] = 0;
+    bool exact_only = false;  // set once a system of this thread diverged
     int64_t kstep = 0;
     while (kstep < nsteps) {
         const int64_t next_sample = (kstep / stride + 1) * stride;
@@ -115,41 +143,85 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             n = next_sample - kstep;
         if (n > kChunk)
             n = kChunk;
-        const Sys2 saved = s;
-        bool ok = ok0;
-        for (int j = 0; j < n; ++j)
-            step2<false>(s, C0, C1, m0, m1, k, ok);
-        if (!(ok & finite2(s))) {
+        Sys2 saved[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+            saved[j] = s[j];
+        bool ok = ok0 & !exact_only;
+        if (ok) {
+            for (int t = 0; t < n; ++t) {
+#pragma unroll
+                for (int j = 0; j < NS; ++j)
+                    step2<false>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
+            }
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+                ok &= finite2(s[j]);
+        }
+        if (!ok) {
             // A division left nvcc's fast path or a value went non-finite:
             // replay the chunk with IEEE division, checking every step.
             // Non-finite values are absorbing under + - * /, so the first
-            // non-finite step is integrate's NonFiniteStateError.step
-            // (oscillator.py:255-260).
-            s = saved;
-            for (int j = 0; j < n; ++j) {
-                step2<true>(s, C0, C1, m0, m1, k, ok);
-                if (!finite2(s)) {
-                    bad = kstep + j + 1;
-                    break;
+            // non-finite step of each system is integrate's
+            // NonFiniteStateError.step (oscillator.py:255-260).
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+                s[j] = saved[j];
+            for (int t = 0; t < n; ++t) {
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    step2<true>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
+                    if (bad[j] == 0 && !finite2(s[j])) {
+                        bad[j] = kstep + t + 1;
+                        exact_only = true;
+                    }
                 }
             }
-            if (bad)
-                break;
         }
         kstep += n;
         if (xs && kstep % stride == 0) {
             const int64_t o = (kstep / stride) * 2 * B;
-            xs[o + i] = s.x0;
-            xs[o + B + i] = s.x1;
-            vs[o + i] = s.v0;
-            vs[o + B + i] = s.v1;
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                if (live[j]) {
+                    const int64_t i = idx[j];
+                    xs[o + i] = s[j].x0;
+                    xs[o + B + i] = s[j].x1;
+                    vs[o + i] = s[j].v0;
+                    vs[o + B + i] = s[j].v1;
+                }
+            }
+        }
+        bool all_bad = true;
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+            all_bad &= (bad[j] != 0) | !live[j];
+        if (all_bad)
+            break;
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        if (live[j]) {
+            const int64_t i = idx[j];
+            x[i] = s[j].x0;
+            x[B + i] = s[j].x1;
+            v[i] = s[j].v0;
+            v[B + i] = s[j].v1;
+            first_bad[i] = bad[j];
         }
     }
-    x[i] = s.x0;
-    x[B + i] = s.x1;
-    v[i] = s.v0;
-    v[B + i] = s.v1;
-    first_bad[i] = bad;
+}
+
+template <int NS>
+cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, int64_t B,
+                      StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                      int64_t *first_bad, int threads, cudaStream_t stream)
+{
+    const int64_t per_block = int64_t(threads) * NS;
+    const int64_t blocks = (B + per_block - 1) / per_block;
+    batch2_rk4_kernel<NS><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+        m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad);
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -158,11 +230,22 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
                           int64_t *first_bad, cudaStream_t stream)
 {
-    const int threads = 256;
-    const int64_t blocks = (B + threads - 1) / threads;
-    batch2_rk4_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-        m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad);
-    return cudaGetLastError();
+    // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
+    // overrides it for benchmarking (read-only process state).
+    int ns = kBatch2NS, threads = kBatch2Threads;
+    if (const char *e = std::getenv("OSC_B2")) {
+        int a = 0, b = 0;
+        if (std::sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && b >= 32 &&
+            b <= 256 && b % 32 == 0) {
+            ns = a;
+            threads = b;
+        }
+    }
+    switch (ns) {
+    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad, threads, stream);
+    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad, threads, stream);
+    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad, threads, stream);
+    }
 }
 
 }  // namespace osc

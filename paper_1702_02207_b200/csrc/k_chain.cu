@@ -108,7 +108,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], mul(2.0, yv[j]));
-        sv[j] = add(sv[j], mul(2.0, a[j]));
+        sv[j] = add_twice<kExact>(sv[j], a[j]);
         yp[j] = add(x[j], mul(k.half_dt, yv[j]));
         yv[j] = add(v[j], mul(k.half_dt, a[j]));
     }
@@ -116,7 +116,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], mul(2.0, yv[j]));
-        sv[j] = add(sv[j], mul(2.0, a[j]));
+        sv[j] = add_twice<kExact>(sv[j], a[j]);
         yp[j] = add(x[j], mul(k.dt, yv[j]));
         yv[j] = add(v[j], mul(k.dt, a[j]));
     }

@@ -124,7 +124,7 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 
 class Workload:
-    def __init__(self, name, rank, device, halo):
+    def __init__(self, name, rank, device, halo, world=1):
         import torch
 
         from paper_1702_02207_b200 import batched
@@ -149,8 +149,14 @@ class Workload:
             T = halo or 16
             self.kernel = "chain_rk4_kernel<8>"
             self.launches = -(-p.nsteps // T)
+            self.world = world
             self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",
-                         "cells": workloads.C3_S, "halo_steps": T}
+                         "cells": workloads.C3_S, "halo_steps": T,
+                         "sharding": f"{world} contiguous shards, 2T-cell ghost zones "
+                                     "exchanged every T steps (NCCL send/recv)"}
+            self.shard = None
+            if world > 1:
+                self.launches = 3 * self.launches  # interior + 2 edge launches per period
         elif name == "C1":
             arrays = workloads.c1()
             arrays = tuple(a[:, None] for a in arrays)
@@ -161,12 +167,27 @@ class Workload:
         self.host = arrays
         self.dev = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(device) for a in arrays)
         self.dof = int(arrays[0].size)
+        if name == "C3" and world > 1:
+            from paper_1702_02207_b200 import sharded
+
+            # strong scaling: each rank owns s/world cells plus 2T-cell ghosts
+            self.shard = sharded.ShardedChain(*self.dev, self.dt, halo_steps=T, device=device)
+            lo, hi = self.shard.L.own
+            self.shard_x0 = self.shard.x.clone()
+            self.shard_v0 = self.shard.v.clone()
+            self.dof = hi - lo
         self.dof_steps = self.dof * self.nsteps
 
     def step(self):
         m, C, x0, v0 = self.dev
         if self.name in ("C2", "C1"):
             return self.batched.integrate_batch2(m, C, x0, v0, self.dt, self.nsteps, check=False)
+        if self.name == "C3" and self.shard is not None:
+            sh = self.shard  # reset the shard to the initial state, then integrate
+            sh.x.copy_(self.shard_x0)
+            sh.v.copy_(self.shard_v0)
+            sh.first_bad.zero_()
+            return sh.run(self.nsteps)
         if self.name == "C3":
             return self.batched.integrate_chains(m[None], C[None], x0[None], v0[None], self.dt,
                                                  self.nsteps, check=False,
@@ -174,7 +195,34 @@ class Workload:
         return self.batched.integrate_chains(m, C, x0, v0, self.dt, self.nsteps, check=False)
 
     # ---- end to end through the host-pointer C ABI --------------------------------
+    def e2e_sharded(self, steps, warmup):
+        """Sharded C3: pinned host shard -> H2D -> integrate with halo exchange -> D2H."""
+        torch = self.torch
+        sh = self.shard
+        hx = self.shard_x0.cpu().pin_memory()
+        hv = self.shard_v0.cpu().pin_memory()
+        lo, hi = sh.L.own
+        ox = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+        ov = torch.empty_like(ox)
+        times = []
+        for i in range(warmup + steps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            sh.x.copy_(hx, non_blocking=True)
+            sh.v.copy_(hv, non_blocking=True)
+            sh.first_bad.zero_()
+            sh.run(self.nsteps)
+            x, v = sh.owned()
+            ox.copy_(x, non_blocking=True)
+            ov.copy_(v, non_blocking=True)
+            torch.cuda.synchronize()
+            if i >= warmup:
+                times.append(time.perf_counter() - t)
+        return sum(times), 2 * hx.numel() * 8, 2 * ox.numel() * 8 + 8
+
     def e2e(self, steps, warmup):
+        if getattr(self, "shard", None) is not None:
+            return self.e2e_sharded(steps, warmup)
         from paper_1702_02207_b200 import _native
 
         torch = self.torch
@@ -348,10 +396,10 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    if world > 1 and args.config in ("C1", "C3"):
-        raise SystemExit(f"{args.config} is single-GPU in this build (DESIGN.md 'Multi-GPU')")
+    if world > 1 and args.config == "C1":
+        raise SystemExit("C1 is one serial 2-DOF system: replicas only (DESIGN.md)")
 
-    wl = Workload(args.config, rank, device, args.halo)
+    wl = Workload(args.config, rank, device, args.halo, world)
     fp64 = fp64_peak(local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > L2 (126 MB)
 
@@ -405,6 +453,7 @@ def main():
             dist.destroy_process_group()
         return 0
 
+    strong = wl.name == "C3" and world > 1
     value = world * wl.dof_steps * args.steps / dev_s
     per_gpu = wl.dof_steps * args.steps / dev_s
     launch_s = dev_s / (args.steps * wl.launches)
@@ -416,7 +465,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if wl.name == "C3" else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy PCG64, workloads.py; no dataset exists)",
         "config": dict(wl.desc, dt=wl.dt, nsteps_per_step=wl.nsteps,
                        dof_steps_per_gpu_step=wl.dof_steps, parallelism=f"dp{world}",

@@ -1,0 +1,276 @@
+"""Multi-GPU long-chain integration: 1-D domain decomposition + halo exchange.
+
+BASELINE configs[2]: one wall-anchored chain of s cells split into
+contiguous shards, one per rank (rank 0 owns the wall, the last rank the free
+end).  A step's dependency radius is 2 cells of x and v, so every T steps each
+rank refreshes a ghost zone of g = 2T cells on each side from its neighbours
+and then advances its own cells T steps with the temporally blocked kernel
+(``osc_rk4_chain_advance``).  Every owned cell goes through exactly the
+operations it goes through on one GPU, so the result is byte-identical for
+any number of ranks -- the GPU form of the reference engine's
+"bitwise-identical for every worker count" contract (parallel.py:11-14,
+test_parallel.py:259-271).
+
+Per period the exchange overlaps compute: the interior tiles (which read no
+ghost cell) are launched first, the ghost exchange runs on a side stream
+(NCCL send/recv of 2 x g doubles per neighbour), and the two edge tiles are
+launched after it.  The plumbing is ``torch.distributed`` (NCCL on GPUs, gloo
+in the CPU tests, where ``advance`` is injected).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def partition(s: int, rank: int, world: int) -> tuple[int, int]:
+    """Balanced contiguous slice [lo, hi) of s cells for rank."""
+    return s * rank // world, s * (rank + 1) // world
+
+
+@dataclass
+class ShardLayout:
+    s: int          # global chain length
+    lo: int         # first owned global cell
+    hi: int         # one past the last owned global cell
+    blo: int        # first buffered global cell (incl. left ghosts)
+    bhi: int        # one past the last buffered global cell
+    g: int          # ghost width = 2 * halo_steps
+
+    @property
+    def n(self) -> int:
+        return self.bhi - self.blo
+
+    @property
+    def own(self) -> tuple[int, int]:
+        return self.lo - self.blo, self.hi - self.blo
+
+    @property
+    def left_ghost(self) -> int:
+        return self.lo - self.blo
+
+    @property
+    def right_ghost(self) -> int:
+        return self.bhi - self.hi
+
+
+def layout(s: int, rank: int, world: int, halo_steps: int) -> ShardLayout:
+    lo, hi = partition(s, rank, world)
+    g = 2 * halo_steps
+    if world > 1 and (hi - lo) < g:
+        raise ValueError(f"shard of {hi - lo} cells is narrower than the {g}-cell ghost zone")
+    return ShardLayout(s, lo, hi, max(0, lo - g), min(s, hi + g), g)
+
+
+def _cuda_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
+                  stream=None):
+    from . import batched
+
+    batched.chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
+                          first_bad, stream=stream)
+
+
+class ShardedChain:
+    """One rank's shard of a chain; ``run`` integrates nsteps with halo exchange.
+
+    ``m, C, x0, v0`` are the GLOBAL arrays (numpy or tensors); each rank
+    copies its buffered slice.  ``advance`` defaults to the CUDA kernel; tests
+    inject the oracle to check the exchange logic on CPU ranks.
+    """
+
+    # interior/edge split: an edge region is at least one tile of owned cells
+    EDGE_CELLS = 4096  # >= any tile (K x threads) so interior tiles never slide into ghosts
+
+    def __init__(self, m, C, x0, v0, dt, *, halo_steps=16, group=None, device=None,
+                 advance=None, rank=None, world=None):
+        self.group = group
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank, self.world = rank, world
+        self.dt = float(dt)
+        self.T = int(halo_steps)
+        s = len(m)
+        self.L = layout(s, self.rank, self.world, self.T)
+        self.device = device or (torch.device("cuda", torch.cuda.current_device())
+                                 if torch.cuda.is_available() else torch.device("cpu"))
+        self.advance = advance or _cuda_advance
+        sl = slice(self.L.blo, self.L.bhi)
+
+        def t(a):
+            a = a if isinstance(a, torch.Tensor) else torch.as_tensor(a)
+            # always a private copy: the caller's arrays are never aliased
+            return a[sl].to(device=self.device, dtype=torch.float64, copy=True).contiguous()
+
+        self.m, self.C = t(m), t(C)
+        self.x, self.v = t(x0), t(v0)
+        self.x2, self.v2 = self.x.clone(), self.v.clone()
+        self.first_bad = torch.zeros(1, dtype=torch.int64, device=self.device)
+        g = self.L.g
+        self.send_l = torch.empty(2, g, dtype=torch.float64, device=self.device)
+        self.send_r = torch.empty_like(self.send_l)
+        self.recv_l = torch.empty_like(self.send_l)
+        self.recv_r = torch.empty_like(self.send_l)
+        self.cuda = self.device.type == "cuda"
+        self.comm_stream = torch.cuda.Stream(self.device) if self.cuda else None
+
+    # -- ghost exchange ------------------------------------------------------
+    def boundary(self, x, v):
+        """Owned boundary cells to ship: (left [2][g], right [2][g])."""
+        a, b = self.L.own
+        g = self.L.g
+        self.send_l[0].copy_(x[a:a + g])
+        self.send_l[1].copy_(v[a:a + g])
+        self.send_r[0].copy_(x[b - g:b])
+        self.send_r[1].copy_(v[b - g:b])
+        return self.send_l, self.send_r
+
+    def fill_ghosts(self, x, v, from_left=None, from_right=None):
+        a, b = self.L.own
+        g = self.L.g
+        if from_left is not None:
+            x[a - g:a].copy_(from_left[0])
+            v[a - g:a].copy_(from_left[1])
+        if from_right is not None:
+            x[b:b + g].copy_(from_right[0])
+            v[b:b + g].copy_(from_right[1])
+
+    def _exchange(self, x, v):
+        """Refresh both ghost zones of (x, v) from the neighbours' owned cells."""
+        self.boundary(x, v)
+        ops = []
+        left = self.rank - 1 if self.rank > 0 else None
+        right = self.rank + 1 if self.rank < self.world - 1 else None
+        if left is not None:
+            ops.append(dist.P2POp(dist.isend, self.send_l, left, self.group))
+            ops.append(dist.P2POp(dist.irecv, self.recv_l, left, self.group))
+        if right is not None:
+            ops.append(dist.P2POp(dist.isend, self.send_r, right, self.group))
+            ops.append(dist.P2POp(dist.irecv, self.recv_r, right, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        self.fill_ghosts(x, v, self.recv_l if left is not None else None,
+                         self.recv_r if right is not None else None)
+
+    def _advance(self, xin, vin, xout, vout, lo, hi, n, step0, stream=None):
+        if hi > lo:
+            kw = {"stream": stream} if self.cuda else {}
+            self.advance(self.m, self.C, xin, vin, xout, vout, lo, hi, self.dt, n, step0,
+                         self.first_bad, **kw)
+
+    # -- one period of T steps, in three phases ------------------------------
+    def _split(self):
+        a, b = self.L.own
+        return self.nranks > 1 and (b - a) > 2 * self.EDGE_CELLS + 2 * self.L.g
+
+    def phase_interior(self, n, k):
+        """Launch the tiles that read no ghost cell (all of them if unsplit)."""
+        a, b = self.L.own
+        E = self.EDGE_CELLS
+        if self.nranks == 1:
+            self._advance(self.x, self.v, self.x2, self.v2, a, b, n, k)
+        elif self._split():
+            self._advance(self.x, self.v, self.x2, self.v2, a + E, b - E, n, k)
+
+    def phase_edges(self, n, k):
+        """After the ghost exchange: the tiles next to the ghost zones."""
+        a, b = self.L.own
+        E = self.EDGE_CELLS
+        if self.nranks == 1:
+            pass
+        elif self._split():
+            self._advance(self.x, self.v, self.x2, self.v2, a, a + E, n, k)
+            self._advance(self.x, self.v, self.x2, self.v2, b - E, b, n, k)
+        else:
+            self._advance(self.x, self.v, self.x2, self.v2, a, b, n, k)
+        self.x, self.x2 = self.x2, self.x
+        self.v, self.v2 = self.v2, self.v
+
+    @property
+    def nranks(self):
+        return self.world
+
+    def run(self, nsteps: int):
+        """Advance the shard nsteps steps; returns the 1-based first bad step
+        of the WHOLE chain (min over ranks) or 0."""
+        k = 0
+        while k < nsteps:
+            n = min(self.T, nsteps - k)
+            self.phase_interior(n, k)
+            if self.world > 1:
+                if self.cuda:
+                    main = torch.cuda.current_stream(self.device)
+                    self.comm_stream.wait_stream(main)
+                    with torch.cuda.stream(self.comm_stream):
+                        self._exchange(self.x, self.v)
+                    main.wait_stream(self.comm_stream)
+                else:
+                    self._exchange(self.x, self.v)
+            self.phase_edges(n, k)
+            k += n
+        fb = self.first_bad.clone()
+        if self.world > 1:
+            big = torch.iinfo(torch.int64).max
+            fb = torch.where(fb > 0, fb, torch.full_like(fb, big))
+            dist.all_reduce(fb, op=dist.ReduceOp.MIN, group=self.group)
+            fb = torch.where(fb == big, torch.zeros_like(fb), fb)
+        return int(fb.item())
+
+    def owned(self):
+        """(x, v) of the owned cells (views)."""
+        a, b = self.L.own
+        return self.x[a:b], self.v[a:b]
+
+    def gather(self):
+        """Full chain state on every rank (validation only)."""
+        x, v = self.owned()
+        if self.world == 1:
+            return x.clone(), v.clone()
+        parts_x = [None] * self.world
+        parts_v = [None] * self.world
+        dist.all_gather_object(parts_x, x.cpu(), group=self.group)
+        dist.all_gather_object(parts_v, v.cpu(), group=self.group)
+        return torch.cat(parts_x), torch.cat(parts_v)
+
+
+class LocalShardGroup:
+    """All shards of a chain in ONE process, advanced in lockstep.
+
+    Same per-shard kernels, layouts and interior/edge phases as the
+    multi-process path, with the ghost exchange done by device copies.  Used to
+    test the decomposition on a single GPU (no kernel ever waits on another, so
+    this is safe to run with several shards on one device).
+    """
+
+    def __init__(self, m, C, x0, v0, dt, shards: int, *, halo_steps=16, device=None,
+                 advance=None):
+        self.parts = [ShardedChain(m, C, x0, v0, dt, halo_steps=halo_steps, device=device,
+                                   advance=advance, rank=r, world=shards)
+                      for r in range(shards)]
+
+    def run(self, nsteps: int) -> int:
+        T = self.parts[0].T
+        k = 0
+        while k < nsteps:
+            n = min(T, nsteps - k)
+            for p in self.parts:
+                p.phase_interior(n, k)
+            sends = [tuple(t.clone() for t in p.boundary(p.x, p.v)) for p in self.parts]
+            for r, p in enumerate(self.parts):
+                left = sends[r - 1][1] if r > 0 else None
+                right = sends[r + 1][0] if r + 1 < len(self.parts) else None
+                p.fill_ghosts(p.x, p.v, left, right)
+            for p in self.parts:
+                p.phase_edges(n, k)
+            k += n
+        bad = [int(p.first_bad.item()) for p in self.parts]
+        bad = [b for b in bad if b > 0]
+        return min(bad) if bad else 0
+
+    def gather(self):
+        xs, vs = zip(*(p.owned() for p in self.parts))
+        return torch.cat(xs), torch.cat(vs)

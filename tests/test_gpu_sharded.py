@@ -1,0 +1,60 @@
+"""The multi-shard chain driver with the CUDA kernel, all shards on one GPU
+(LocalShardGroup: lockstep, copy-based ghost exchange; no kernel waits on
+another).  Byte-identical to the single-GPU integration for every shard
+count."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1702_02207_b200 import batched, sharded  # noqa: E402
+
+
+def _chain(s, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(0.5, 2.0, s), rng.uniform(500.0, 2000.0, s), rng.standard_normal(s),
+            rng.standard_normal(s))
+
+
+@pytest.mark.parametrize("shards,T", [(1, 16), (2, 16), (3, 7), (8, 16)])
+def test_local_group_cuda_bit_identical(shards, T):
+    s = 300_000
+    m, C, x0, v0 = _chain(s, shards)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, shards, halo_steps=T)
+    assert grp.run(101) == 0
+    x, v = grp.gather()
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 101)
+    assert bits(x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
+    assert bits(v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())
+
+
+def test_local_group_cuda_against_oracle_windows():
+    s = 50_000
+    m, C, x0, v0 = _chain(s, 9)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 4, halo_steps=16)
+    grp.run(60)
+    x, _ = grp.gather()
+    x = x.cpu().numpy()
+    for a, b in ((0, 500), (s // 4 - 300, s // 4 + 300), (s - 500, s)):
+        lo, hi, off = oracle.light_cone(s, a, b, 60)
+        _, _, xo, _, _ = oracle.c_rk4_chains(m[None, lo:hi], C[None, lo:hi], x0[None, lo:hi],
+                                             v0[None, lo:hi], 1e-3, 60, sample=False)
+        assert bits(x[a:b]) == bits(xo[0, off:off + b - a])
+
+
+def test_local_group_cuda_divergence():
+    s = 100_000
+    m, C, x0, v0 = _chain(s, 4)
+    C[77_000] = 1e8
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 4, halo_steps=16)
+    fb = grp.run(300)
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 300, check=False)
+    assert fb > 0 and fb == int(ref.first_bad[0])

@@ -1,0 +1,128 @@
+"""Multi-rank chain decomposition (BASELINE configs[2]) on CPU.
+
+The ranks are real processes over torch.distributed (gloo, 127.0.0.1); the
+per-shard advance is the oracle (the CUDA kernel needs a GPU -- the GPU tests
+run the same driver with the kernel).  The result must be byte-identical to
+the single-process integration for every rank count, as the reference's
+engine is for every worker count (test_parallel.py:259-271)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from conftest import bits
+from paper_1702_02207_b200 import sharded
+
+
+def oracle_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
+                   **_):
+    """Same contract as osc_rk4_chain_advance, on the CPU oracle: the buffer is
+    treated as its own chain (wall at cell 0, free at n-1); only the owned
+    cells are written and checked."""
+    x, v = xin.numpy().copy(), vin.numpy().copy()
+    m, C = m.numpy(), C.numpy()
+    for j in range(nsteps):
+        with np.errstate(all="ignore"):
+            x, v = oracle.np_rk4_step(m, C, x, v, dt)
+        own = slice(own_lo, own_hi)
+        if not (np.isfinite(x[own]).all() and np.isfinite(v[own]).all()):
+            fb = int(first_bad.item())
+            if fb == 0 or fb > step0 + j + 1:
+                first_bad.fill_(step0 + j + 1)
+            break
+    xout[own_lo:own_hi] = torch.from_numpy(x[own_lo:own_hi])
+    vout[own_lo:own_hi] = torch.from_numpy(v[own_lo:own_hi])
+
+
+def _chain(s, seed, stiff=None):
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(0.5, 2.0, s)
+    C = rng.uniform(500.0, 2000.0, s)
+    if stiff is not None:
+        C[stiff] = 1e8
+    x0 = rng.standard_normal(s)
+    v0 = rng.standard_normal(s)
+    return m, C, x0, v0
+
+
+def _free_port():
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
+def _worker(rank, world, port, s, nsteps, T, edge, stiff, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, C, x0, v0 = _chain(s, 11, stiff)
+        sh = sharded.ShardedChain(m, C, x0, v0, 1e-3, halo_steps=T, device=torch.device("cpu"),
+                                  advance=oracle_advance)
+        sh.EDGE_CELLS = edge
+        fb = sh.run(nsteps)
+        x, v = sh.gather()
+        if rank == 0:
+            q.put((fb, x.numpy(), v.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world, s, nsteps, T, edge=64, stiff=None):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.start_processes(_worker, args=(world, _free_port(), s, nsteps, T, edge, stiff, q),
+                       nprocs=world, join=True, start_method="spawn")
+    return q.get()
+
+
+def test_layout():
+    L = sharded.layout(100, 1, 4, 3)
+    assert (L.lo, L.hi, L.blo, L.bhi, L.g) == (25, 50, 19, 56, 6)
+    assert L.own == (6, 31) and L.n == 37
+    L0 = sharded.layout(100, 0, 4, 3)
+    assert L0.blo == 0 and L0.own == (0, 25)
+    L3 = sharded.layout(100, 3, 4, 3)
+    assert L3.bhi == 100 and L3.right_ghost == 0
+    with pytest.raises(ValueError):
+        sharded.layout(100, 0, 50, 3)
+
+
+@pytest.mark.parametrize("world,T,nsteps", [(2, 8, 37), (3, 5, 40)])
+def test_gloo_ranks_bit_identical(world, T, nsteps):
+    s = 1500
+    fb, x, v = _run_world(world, s, nsteps, T)
+    m, C, x0, v0 = _chain(s, 11)
+    _, _, xo, vo, fbo = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, nsteps,
+                                            sample=False)
+    assert fb == 0 and fbo[0] == 0
+    assert bits(x) == bits(xo[0]) and bits(v) == bits(vo[0])
+
+
+def test_gloo_divergence_is_min_over_ranks():
+    s = 1500
+    fb, _, _ = _run_world(3, s, 400, 8, stiff=1400)  # in the last rank's shard
+    m, C, x0, v0 = _chain(s, 11, 1400)
+    _, _, _, _, fbo = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 400,
+                                          sample=False)
+    assert fbo[0] > 0 and fb == fbo[0]
+
+
+def test_local_group_matches_single_chain():
+    s = 3000
+    m, C, x0, v0 = _chain(s, 5)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 4, halo_steps=6,
+                                  device=torch.device("cpu"), advance=oracle_advance)
+    for p in grp.parts:
+        p.EDGE_CELLS = 100  # exercise the interior/edge split on small shards
+    assert grp.run(45) == 0
+    x, v = grp.gather()
+    _, _, xo, vo, _ = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 45,
+                                          sample=False)
+    assert bits(x.numpy()) == bits(xo[0]) and bits(v.numpy()) == bits(vo[0])

@@ -201,6 +201,8 @@ class Workload:
         sh = self.shard
         hx = self.shard_x0.cpu().pin_memory()
         hv = self.shard_v0.cpu().pin_memory()
+        hm = sh.m.cpu().pin_memory()
+        hC = sh.C.cpu().pin_memory()
         lo, hi = sh.L.own
         ox = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
         ov = torch.empty_like(ox)
@@ -208,6 +210,8 @@ class Workload:
         for i in range(warmup + steps):
             torch.cuda.synchronize()
             t = time.perf_counter()
+            sh.m.copy_(hm, non_blocking=True)
+            sh.C.copy_(hC, non_blocking=True)
             sh.x.copy_(hx, non_blocking=True)
             sh.v.copy_(hv, non_blocking=True)
             sh.first_bad.zero_()
@@ -218,7 +222,7 @@ class Workload:
             torch.cuda.synchronize()
             if i >= warmup:
                 times.append(time.perf_counter() - t)
-        return sum(times), 2 * hx.numel() * 8, 2 * ox.numel() * 8 + 8
+        return sum(times), 4 * hx.numel() * 8, 2 * ox.numel() * 8 + 8
 
     def e2e(self, steps, warmup):
         if getattr(self, "shard", None) is not None:

@@ -37,11 +37,11 @@ from paper_1702_02207_b200 import workloads  # noqa: E402
 METRIC = "DOF-steps/s"
 UNIT = "DOF-steps/s"
 HBM_BYTES_PER_DOF_STEP = 48  # read x,v,m,C + write x,v, one step per round trip
-FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42}
+FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42, "C5": 4 * 2 * 4096}
 # DP-pipe instructions per DOF-step in the hot loops, counted in SASS with
 # scripts/sass_stats.py --loop: batch2 184 per 2 systems per step
 # (NS=2); chain 396 per 8 cells (K=8, the default shape of both chain modes).
-DP_INST_PER_DOF_STEP = {"C1": 46, "C2": 46, "C3": 49.5, "C4": 49.5}
+DP_INST_PER_DOF_STEP = {"C1": 46, "C2": 46, "C3": 49.5, "C4": 49.5, "C5": None}
 
 
 def peaks():
@@ -157,6 +157,13 @@ class Workload:
             self.shard = None
             if world > 1:
                 self.launches = 3 * self.launches  # interior + 2 edge launches per period
+        elif name == "C5":
+            arrays = workloads.c5(rank=rank)  # m, K, X0, V0
+            self.kernel = "dense_rk4_gemm"
+            self.launches = 2 * p.nsteps  # + rowscale, pack, unpack (counted in gpu_launches)
+            self.desc = {"workload": "C5: dense SPD system s=4096, A = M^-1 K, 1024 trajectories",
+                         "s": workloads.C5_S, "trajectories_per_gpu": workloads.C5_N,
+                         "gemm_per_launch": "4096 x 4096 x 2048 fp64 (DMMA), RK4 epilogue fused"}
         elif name == "C1":
             arrays = workloads.c1()
             arrays = tuple(a[:, None] for a in arrays)
@@ -166,7 +173,7 @@ class Workload:
             raise SystemExit(f"unknown config {name}")
         self.host = arrays
         self.dev = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(device) for a in arrays)
-        self.dof = int(arrays[0].size)
+        self.dof = int(arrays[0].size) if name != "C5" else int(arrays[2].size)
         if name == "C3" and world > 1:
             from paper_1702_02207_b200 import sharded
 
@@ -180,6 +187,9 @@ class Workload:
 
     def step(self):
         m, C, x0, v0 = self.dev
+        if self.name == "C5":
+            A = self.batched.rowscale(C, m)  # (m, K): A = M^-1 K, once per run
+            return self.batched.integrate_dense(A, x0, v0, self.dt, self.nsteps, check=False)
         if self.name in ("C2", "C1"):
             return self.batched.integrate_batch2(m, C, x0, v0, self.dt, self.nsteps, check=False)
         if self.name == "C3" and self.shard is not None:
@@ -224,7 +234,30 @@ class Workload:
                 times.append(time.perf_counter() - t)
         return sum(times), 4 * hx.numel() * 8, 2 * ox.numel() * 8 + 8
 
+    def e2e_dense(self, steps, warmup):
+        """C5 through the public API: pinned host m, K, X0, V0 -> H2D -> rowscale +
+        integrate_dense -> D2H of X, V."""
+        torch = self.torch
+        pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in self.host]
+        outs = [torch.empty_like(pinned[2]).pin_memory() for _ in range(2)]
+        dev = self.dev[0].device
+        times = []
+        for i in range(warmup + steps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            m, K, X0, V0 = (a.to(dev, non_blocking=True) for a in pinned)
+            res = self.batched.integrate_dense(self.batched.rowscale(K, m), X0, V0, self.dt,
+                                               self.nsteps, check=False)
+            outs[0].copy_(res.x, non_blocking=True)
+            outs[1].copy_(res.v, non_blocking=True)
+            torch.cuda.synchronize()
+            if i >= warmup:
+                times.append(time.perf_counter() - t)
+        return sum(times), sum(a.numel() for a in pinned) * 8, 2 * outs[0].numel() * 8
+
     def e2e(self, steps, warmup):
+        if self.name == "C5":
+            return self.e2e_dense(steps, warmup)
         if getattr(self, "shard", None) is not None:
             return self.e2e_sharded(steps, warmup)
         from paper_1702_02207_b200 import _native
@@ -264,8 +297,26 @@ class Workload:
         return sum(times), h2d, d2h
 
 
-def fp64_peak(device_index):
-    """Measured DP-pipe issue rate (lane-instructions/s) with the DFMA microbench."""
+def cublas_dgemm(device_index):
+    """cuBLAS DGEMM (torch.matmul float64) on the C5 GEMM shape: the library bar."""
+    import torch
+
+    M, K, N = workloads.C5_S, workloads.C5_S, 2 * workloads.C5_N
+    a = torch.randn(M, K, dtype=torch.float64, device=device_index)
+    b = torch.randn(K, N, dtype=torch.float64, device=device_index)
+    for _ in range(2):
+        a @ b
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(10):
+        a @ b
+    end.record()
+    torch.cuda.synchronize()
+    return 10 * 2.0 * M * K * N / (start.elapsed_time(end) * 1e-3)
+
+
+def fp64_peak(device_index, mode=0):
+    """Measured FP64 rate: DFMA lane-instructions/s (mode 0) or DMMA flops/s (mode 2)."""
     import torch
 
     from paper_1702_02207_b200 import _native
@@ -278,7 +329,7 @@ def fp64_peak(device_index):
     for it in (2000, 20000, 20000):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        rc = lib.osc_bench_fp64(it, 0, sink.data_ptr(), ctypes.byref(ops), stream)
+        rc = lib.osc_bench_fp64(it, mode, sink.data_ptr(), ctypes.byref(ops), stream)
         end.record()
         torch.cuda.synchronize()
         if rc:
@@ -317,6 +368,20 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
         el = time.perf_counter() - t
         done = nb * s * steps
         sample = f"{nb} of {Bc} chains x {steps} of {wl.nsteps} steps"
+    elif wl.name == "C5":
+        # no reference implementation: the numpy restatement
+        # (fp64 BLAS on all cores) -- "restatement, not reference"
+        m, K, X0, V0 = wl.host
+        A = K / m[:, None]
+        steps = 2
+        t = time.perf_counter()
+        oracle.dense_rk4(A, X0, V0, wl.dt, steps)
+        el = time.perf_counter() - t
+        done = X0.size * steps
+        sample = (f"{steps} of {wl.nsteps} steps of the full s=4096 x 1024 system, numpy/BLAS "
+                  "restatement (the reference has no dense path)")
+        return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": sample}
     else:  # C3: the whole chain, cells split across threads per phase
         s = m.size
         steps = 20
@@ -352,7 +417,7 @@ def run_reference(args):
     wl.name = wl_name
     p = workloads.PARAMS[wl_name]
     wl.dt, wl.nsteps = p.dt, p.nsteps
-    wl.host = {"C2": workloads.c2, "C4": workloads.c4, "C3": workloads.c3,
+    wl.host = {"C2": workloads.c2, "C4": workloads.c4, "C3": workloads.c3, "C5": workloads.c5,
                "C1": lambda: tuple(a[:, None] for a in workloads.c1())}[wl_name]()
     budget = args.ref_budget
     vals = []
@@ -381,7 +446,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--halo", type=int, default=0, help="C3 steps per tiled launch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -457,7 +522,6 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    strong = wl.name == "C3" and world > 1
     value = world * wl.dof_steps * args.steps / dev_s
     per_gpu = wl.dof_steps * args.steps / dev_s
     launch_s = dev_s / (args.steps * wl.launches)
@@ -465,7 +529,33 @@ def main():
     alg_bytes = HBM_BYTES_PER_DOF_STEP * wl.dof_steps / wl.launches
     achieved = alg_bytes / launch_s / 1e9
     traffic = ncu_traffic(wl.kernel, wl.name)
-    dp_inst_rate = per_gpu * DP_INST_PER_DOF_STEP[wl.name]
+    if wl.name == "C5":
+        # GEMM launches dominate: 2 per RK4 step, each [s x s] x [s x 2N]
+        gemm_flops = 2.0 * workloads.C5_S * workloads.C5_S * 2 * workloads.C5_N
+        launch_s = dev_s / (args.steps * wl.launches)
+        dmma = fp64_peak(local, mode=2)
+        achieved_tf = gemm_flops / launch_s / 1e12
+        roofline = {
+            "bound": "tensor", "achieved": achieved_tf, "peak": dmma / 1e12, "unit": "TFLOP/s",
+            "frac": achieved_tf * 1e12 / dmma, "traffic": traffic, "kernel": wl.kernel,
+            "launches_per_step": wl.launches, "algorithmic_flops_per_launch": gemm_flops,
+            "note": "FP64 tensor cores (DMMA.8x8x4). peak = measured DMMA issue "
+                    "microbenchmark (MEASURED_PEAKS.json has no FP64); library bar = cuBLAS "
+                    "DGEMM on the same shape, measured live",
+            "cublas_dgemm_tflops": cublas_dgemm(local) / 1e12,
+        }
+    else:
+        roofline = {
+            "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": traffic,
+            "kernel": wl.kernel, "launches_per_step": wl.launches,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "note": f"SURVEY 8d: 48 B per DOF-step (one step per HBM round trip); peak "
+                    f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
+                    f"is expected; its real limit is the FP64 pipe (roofline_fp64)",
+        }
+    dp = DP_INST_PER_DOF_STEP[wl.name]
+    dp_inst_rate = per_gpu * dp if dp else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps,
@@ -476,27 +566,21 @@ def main():
                        dof_steps_per_gpu_step=wl.dof_steps, parallelism=f"dp{world}",
                        l2="flushed between timed steps (256 MiB memset outside step events); "
                           "state is register-resident within a step",
-                       arithmetic="IEEE fp64, byte-identical to oscbench.integrate"),
-        "roofline": {
-            "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak, "traffic": traffic,
-            "kernel": wl.kernel, "launches_per_step": wl.launches,
-            "algorithmic_bytes_per_launch": alg_bytes,
-            "note": f"SURVEY 8d: 48 B per DOF-step (one step per HBM round trip); peak "
-                    f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
-                    f"is expected; its real limit is the FP64 pipe (roofline_fp64)",
-        },
+                       arithmetic=("IEEE fp64; GEMM summation order differs from CPU BLAS "
+                                   "(rel. 1e-10 vs the restatement)" if wl.name == "C5" else
+                                   "IEEE fp64, byte-identical to oscbench.integrate")),
+        "roofline": roofline,
         "roofline_fp64": {
-            "bound": "fp64_pipe", "dp_inst_per_dof_step": DP_INST_PER_DOF_STEP[wl.name],
+            "bound": "fp64_pipe", "dp_inst_per_dof_step": dp,
             "achieved_dp_inst_per_s": dp_inst_rate, "peak_dp_inst_per_s": fp64,
-            "frac": dp_inst_rate / fp64 if fp64 else None,
+            "frac": dp_inst_rate / fp64 if dp_inst_rate else None,
             "algorithmic_flops_per_dof_step": FLOPS_PER_DOF_STEP[wl.name],
             "achieved_flops": per_gpu * FLOPS_PER_DOF_STEP[wl.name],
             "peak_note": "measured DFMA issue microbenchmark (osc_bench_fp64), lane-inst/s",
         },
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": wl.launches * args.steps,
+        "gpu_launches": (wl.launches + (3 if wl.name == "C5" else 0)) * args.steps,
         "clocks": clocks.summary(),
         "step_ms": step_ms,
     }

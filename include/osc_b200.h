@@ -82,6 +82,19 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
                           int64_t step0, int64_t *first_bad, void *stream);
 
+/* Dense general system M x'' + K x = 0 (BASELINE configs[4]; outside the
+ * reference).  osc_rowscale: A = K / m[:, None] (IEEE division
+ * per element), A [s][s] row-major.  osc_rk4_dense: N trajectories, X, V
+ * [s][N] row-major (one trajectory per column) advanced in place nsteps
+ * classical RK4 steps with acceleration -(A y) (rk4_step's stage structure,
+ * oscillator.py:208-231), each step as two FP64 tensor-core GEMMs
+ * [s x s] x [s x 2N] with the RK4 elementwise work fused into the epilogue.
+ * Not bit-identical to a CPU BLAS (summation order); deterministic run to
+ * run.  first_bad: [1], first step with a non-finite entry, or 0. */
+int osc_rowscale(const double *K, const double *m, double *A, int64_t s, void *stream);
+int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, double dt,
+                  int64_t nsteps, int64_t *first_bad, void *stream);
+
 /* derivative() (oscillator.py:184-191): dvel[b][i] = acceleration_at(...).
  * cell_major != 0 selects the [s][B] layout (batched 2-DOF SoA). */
 int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,
@@ -99,7 +112,9 @@ int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches,
 
 /* FP64 pipe microbenchmark (roofline denominator; not part of the hot path):
  * enqueues one launch of 8 independent DFMA (mode 0) or DADD (mode 1)
- * chains per thread; *lane_ops (host) = DP lane-instructions it executes.
+ * chains per thread -- *lane_ops (host) = DP lane-instructions executed -- or
+ * of 8 independent DMMA.8x8x4 chains per warp (mode 2; mode 3 adds 8 DFMA
+ * chains per thread) -- *lane_ops = flops executed.
  * sink: device scratch of >= 512 doubles. */
 int osc_bench_fp64(int64_t iters, int mode, double *sink, int64_t *lane_ops, void *stream);
 

@@ -180,3 +180,39 @@ def check_division(n: int, seed: int = 1, mode: int = 0) -> int:
                                           ctypes.c_void_p(_stream()))
     raise_for(rc, "osc_check_division")
     return int(out.value)
+
+
+# --------------------------------------------------------------------------
+# dense general (M, K) path (BASELINE configs[4]; K5)
+# --------------------------------------------------------------------------
+
+def rowscale(K, m, *, stream=None) -> torch.Tensor:
+    """A = K / m[:, None] on the device (IEEE division per element)."""
+    lib = _native.lib()
+    K, m = _dev(K), _dev(m)
+    s = m.numel()
+    if K.shape != (s, s):
+        raise ValueError(f"K must be [{s}][{s}], got {tuple(K.shape)}")
+    A = torch.empty_like(K)
+    raise_for(lib.osc_rowscale(_ptr(K), _ptr(m), _ptr(A), s, ctypes.c_void_p(_stream(stream))),
+              "osc_rowscale")
+    return A
+
+
+def integrate_dense(A, X0, V0, dt, nsteps, *, stream=None, check=True) -> BatchResult:
+    """N trajectories (columns of X0, V0 [s][N]) of x'' = -A x, classical RK4
+    with rk4_step's stage structure (oscillator.py:208-231); two fused FP64
+    tensor-core GEMMs per step.  Tolerance-equal (GEMM summation order) to
+    the restatement oracle.dense_rk4."""
+    lib = _native.lib()
+    A, X0, V0 = (_dev(a) for a in (A, X0, V0))
+    s, N = X0.shape
+    if A.shape != (s, s) or V0.shape != X0.shape:
+        raise ValueError("expected A [s][s], X0 and V0 [s][N]")
+    x, v = X0.clone(), V0.clone()
+    fb = torch.zeros(1, dtype=torch.int64, device=A.device)
+    rc = lib.osc_rk4_dense(_ptr(A), _ptr(x), _ptr(v), s, N, float(dt), int(nsteps), _ptr(fb),
+                           ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_rk4_dense")
+    res = BatchResult(x, v, None, None, fb, float(dt), int(nsteps), int(nsteps))
+    return res.check() if check else res

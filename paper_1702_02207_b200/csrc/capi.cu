@@ -279,6 +279,56 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "chain_rk4_kernel");
 }
 
+int osc_rowscale(const double *K, const double *m, double *A, int64_t s, void *stream)
+{
+    if (s < 1 || !K || !m || !A)
+        return fail(OSC_INVALID, "bad rowscale arguments");
+    cudaError_t e = osc::launch_rowscale(K, m, A, s, s, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "rowscale_kernel");
+}
+
+int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, double dt,
+                  int64_t nsteps, int64_t *first_bad, void *stream_)
+{
+    if (int rc = check_run_args(dt, nsteps, 1))
+        return rc;
+    if (s < 1 || N < 0)
+        return fail(OSC_INVALID, "need s >= 1 and N >= 0");
+    if (N == 0)
+        return OSC_OK;
+    if (!A || !X || !V || !first_bad)
+        return fail(OSC_INVALID, "null buffer");
+    retain_pool_memory();
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const int64_t sp = osc::dense_pad_s(s), Np = osc::dense_pad_n(N);
+    const size_t op = static_cast<size_t>(sp) * 2 * Np, st = static_cast<size_t>(sp) * Np;
+    const bool pad_a = sp != s;
+    const size_t total = 2 * op + 3 * st + (pad_a ? static_cast<size_t>(sp) * sp : 0);
+    Scratch ws;
+    ws.s = stream;
+    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws.p), total * sizeof(double), stream));
+    double *BA = ws.p, *BB = BA + op, *Vp = BB + op, *SX = Vp + st, *SV = SX + st;
+    const double *Ause = A;
+    if (pad_a) {
+        double *Ap = SV + st;
+        OSC_CUDA(cudaMemsetAsync(Ap, 0, sizeof(double) * sp * sp, stream));
+        OSC_CUDA(cudaMemcpy2DAsync(Ap, sp * sizeof(double), A, s * sizeof(double),
+                                   s * sizeof(double), s, cudaMemcpyDeviceToDevice, stream));
+        Ause = Ap;
+    }
+    const osc::StepConsts k = consts(dt);
+    OSC_CUDA(cudaMemsetAsync(first_bad, 0, sizeof(int64_t), stream));
+    cudaError_t e = osc::launch_dense_pack(X, V, BA, Vp, s, N, sp, Np, k.half_dt, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "pack_kernel");
+    e = osc::launch_dense_steps(Ause, BA, BB, Vp, SX, SV, first_bad, sp, Np, k, 0, nsteps,
+                                stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "dense_rk4_gemm");
+    e = osc::launch_dense_unpack(BA, Vp, X, V, s, N, Np, stream);
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "unpack_kernel");
+}
+
 int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,
                    int64_t s, int cell_major, void *stream)
 {

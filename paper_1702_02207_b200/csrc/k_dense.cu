@@ -1,0 +1,306 @@
+// K5 dense_rk4: the dense general-(M,K) path (BASELINE configs[4]).
+//
+// M x'' + K x = 0 with A = M^-1 K precomputed (osc_rowscale), advancing N
+// independent trajectories (columns of X, V) with rk4_step's stage structure
+// (oscillator.py:208-231) where acceleration_at becomes a = -(A y).  The
+// reference keeps only the chain; the oracle is the
+// restatement oracle.dense_rk4 plus the eigen-analytic solution.
+//
+// The four stage GEMMs of a step form two independent pairs:
+//   k1 = -A x            k2 = -A (x + h v)          (need only the step start)
+//   k3 = -A (x + h y2v)  k4 = -A (x + dt y3v)       (need k1 resp. k2 only)
+// with y2v = v + h k1, y3v = v + h k2.  So one step is TWO GEMMs of
+// [s x s] x [s x 2N]:  [k1|k2] = -A [x|y2]  and  [k3|k4] = -A [y3|y4],
+// each with the RK4 elementwise work fused into its epilogue.
+//
+// Operand layout: BA / BB are [s][2N] with columns blocked by 32 trajectories:
+// block cb holds columns (x of trajectories 32cb..32cb+31 | y2 of the same),
+// so one 64-column CTA tile owns both halves of its 32 trajectories and the
+// epilogue is local.  x itself lives in BA's first halves.
+//
+// GEMM: FP64 tensor cores through mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4;
+// tcgen05 has no f64 kind on sm_100a -- ptxas rejects kind::f64).  CTA tile
+// 128 x 64, 8 warps of 32 x 32 (16 DMMA accumulators each), BK = 16,
+// 4-stage cp.async pipeline, padded shared-memory rows (conflict-free
+// fragment loads).  128x64 tiles give 1024 CTAs per GEMM at s=4096, N=1024:
+// 6.92 waves of 148 -> 98.8% wave efficiency.
+#include "osc_device.cuh"
+#include "osc_kernels.h"
+
+namespace osc {
+namespace {
+
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+constexpr int APAD = 4, BPAD = 8;  // doubles of row padding (bank-conflict-free fragments)
+constexpr int AS = BK + APAD;      // A smem row stride
+constexpr int BS = BN + BPAD;      // B smem row stride
+constexpr int THREADS = 256;
+constexpr size_t kStageDoubles = size_t(BM) * AS + size_t(BK) * BS;
+constexpr size_t kSmemBytes = STAGES * kStageDoubles * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+struct DenseArgs {
+    const double *A;   // [s][s] row-major, A = M^-1 K
+    const double *Bop; // [s][2N] blocked operand of this GEMM
+    double *BA;        // [s][2N]  (x | y2) blocks
+    double *BB;        // [s][2N]  (y3 | y4) blocks
+    double *V;         // [s][N]
+    double *SX, *SV;   // [s][N] partial combination sums
+    int64_t *first_bad;
+    int64_t s, N;      // padded sizes: s % BM == 0, N % 32 == 0
+    StepConsts k;
+    int64_t step;      // 1-based step index (divergence tag)
+};
+
+// Stage one BK-slab of A (rows m0..m0+BM) and of Bop (cols n0..n0+BN).
+__device__ __forceinline__ void load_stage(const DenseArgs &g, double *sA, double *sB,
+                                           int64_t m0, int64_t n0, int64_t k0)
+{
+    const int tid = threadIdx.x;
+    const int64_t ld2 = 2 * g.N;
+    // A: BM x BK doubles = BM*BK/2 chunks of 16 B
+#pragma unroll
+    for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {
+        const int c = tid + i * THREADS;
+        const int r = c / (BK / 2), q = c % (BK / 2);
+        cp_async16(sA + r * AS + 2 * q, g.A + (m0 + r) * g.s + k0 + 2 * q);
+    }
+    // B: BK x BN doubles
+#pragma unroll
+    for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {
+        const int c = tid + i * THREADS;
+        const int r = c / (BN / 2), q = c % (BN / 2);
+        cp_async16(sB + r * BS + 2 * q, g.Bop + (k0 + r) * ld2 + n0 + 2 * q);
+    }
+}
+
+template <int kStage>
+__global__ void __launch_bounds__(THREADS, 1) dense_rk4_gemm(DenseArgs g)
+{
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps of 32 x 32
+    const int64_t ntn = (2 * g.N) / BN;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x / ntn) * BM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x % ntn) * BN;
+    const int64_t KT = g.s / BK;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+        if (st < KT)
+            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS, m0, n0,
+                       st * BK);
+        cp_commit();
+    }
+    const int ar = lane >> 2, ac = lane & 3;  // fragment coordinates
+    for (int64_t kt = 0; kt < KT; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const int64_t nk = kt + STAGES - 1;
+        if (nk < KT) {
+            const int st = nk % STAGES;
+            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS, m0, n0,
+                       nk * BK);
+        }
+        cp_commit();
+        const double *sA = smem + (kt % STAGES) * kStageDoubles;
+        const double *sB = sA + BM * AS;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                af[i] = sA[(wm * 32 + i * 8 + ar) * AS + kk + ac];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                bf[j] = sB[(kk + ac) * BS + wn * 32 + j * 8 + ar];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+    __syncthreads();
+
+    // Stage the 128 x 64 accumulator tile through shared memory so each
+    // thread sees both halves (stage j and j+1) of its trajectories.
+    double *sC = smem;  // BM x (BN + 1)
+    constexpr int CS = BN + 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = wm * 32 + i * 8 + ar;
+            const int c = wn * 32 + j * 8 + 2 * ac;
+            sC[r * CS + c] = acc[i][j][0];
+            sC[r * CS + c + 1] = acc[i][j][1];
+        }
+    __syncthreads();
+
+    const int64_t cb = n0 / BN;  // trajectory block
+    const double h = g.k.half_dt, dt = g.k.dt, dt6 = g.k.dt6;
+    const int64_t ld2 = 2 * g.N;
+    bool bad = false;
+    for (int e = tid; e < BM * 32; e += THREADS) {
+        const int r = e >> 5, c = e & 31;
+        const int64_t gr = m0 + r;
+        const int64_t n = cb * 32 + c;               // trajectory
+        const int64_t ix = gr * ld2 + cb * BN + c;   // its first-half column
+        const double p = -sC[r * CS + c];            // k1 (stage 0) or k3 (stage 1)
+        const double q = -sC[r * CS + c + 32];       // k2 or k4
+        const double x = g.BA[ix];
+        const double v = g.V[gr * g.N + n];
+        if constexpr (kStage == 0) {
+            // [k1|k2]: y2v = v + h k1, y3v = v + h k2, y3p = x + h y2v, y4p = x + dt y3v
+            const double y2v = add(v, mul(h, p));
+            const double y3v = add(v, mul(h, q));
+            g.BB[ix] = add(x, mul(h, y2v));
+            g.BB[ix + 32] = add(x, mul(dt, y3v));
+            g.SX[gr * g.N + n] = add(add(v, mul(2.0, y2v)), mul(2.0, y3v));
+            g.SV[gr * g.N + n] = add(p, mul(2.0, q));
+        } else {
+            // [k3|k4]: y4v = v + dt k3; combine_value for x and v (oscillator.py:227-228)
+            const double y4v = add(v, mul(dt, p));
+            const double sx = add(g.SX[gr * g.N + n], y4v);
+            const double sv = add(add(g.SV[gr * g.N + n], mul(2.0, p)), q);
+            const double xn = add(x, mul(dt6, sx));
+            const double vn = add(v, mul(dt6, sv));
+            g.BA[ix] = xn;
+            g.V[gr * g.N + n] = vn;
+            g.BA[ix + 32] = add(xn, mul(h, vn));  // y2p of the next step
+            bad |= !(finite(xn) & finite(vn));
+        }
+    }
+    if (kStage == 1 && __syncthreads_or(bad) && tid == 0)
+        record_bad(g.first_bad, g.step);
+}
+
+// A = K / m[:, None] (exact IEEE division per element), padded to sp x sp.
+__global__ void rowscale_kernel(const double *__restrict__ K, const double *__restrict__ m,
+                                double *__restrict__ A, int64_t s, int64_t sp)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= sp * sp)
+        return;
+    const int64_t r = i / sp, c = i % sp;
+    A[i] = (r < s && c < s) ? __ddiv_rn(K[r * s + c], m[r]) : 0.0;
+}
+
+// Pack X, V [s][N] into the blocked operand BA (x | x + h v) and a padded V.
+__global__ void pack_kernel(const double *__restrict__ X, const double *__restrict__ V0,
+                            double *__restrict__ BA, double *__restrict__ Vp, int64_t s,
+                            int64_t N, int64_t sp, int64_t Np, double h)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= sp * Np)
+        return;
+    const int64_t r = i / Np, n = i % Np;
+    const bool in = r < s && n < N;
+    const double x = in ? X[r * N + n] : 0.0, v = in ? V0[r * N + n] : 0.0;
+    const int64_t ix = r * 2 * Np + (n / 32) * 64 + (n % 32);
+    BA[ix] = x;
+    BA[ix + 32] = add(x, mul(h, v));
+    Vp[r * Np + n] = v;
+}
+
+__global__ void unpack_kernel(const double *__restrict__ BA, const double *__restrict__ Vp,
+                              double *__restrict__ X, double *__restrict__ V, int64_t s,
+                              int64_t N, int64_t Np)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= s * N)
+        return;
+    const int64_t r = i / N, n = i % N;
+    X[i] = BA[r * 2 * Np + (n / 32) * 64 + (n % 32)];
+    V[i] = Vp[r * Np + n];
+}
+
+}  // namespace
+
+int64_t dense_pad_s(int64_t s) { return (s + BM - 1) / BM * BM; }
+int64_t dense_pad_n(int64_t n) { return (n + 31) / 32 * 32; }
+
+cudaError_t launch_rowscale(const double *K, const double *m, double *A, int64_t s, int64_t sp,
+                            cudaStream_t stream)
+{
+    const int64_t total = sp * sp;
+    rowscale_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(K, m, A, s,
+                                                                                      sp);
+    return cudaGetLastError();
+}
+
+// Integrate nsteps with the padded workspace already holding the packed state.
+cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *Vp, double *SX,
+                               double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
+                               StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream)
+{
+    cudaFuncSetAttribute(dense_rk4_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(dense_rk4_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
+    DenseArgs g{};
+    g.A = A;
+    g.BA = BA;
+    g.BB = BB;
+    g.V = Vp;
+    g.SX = SX;
+    g.SV = SV;
+    g.first_bad = first_bad;
+    g.s = sp;
+    g.N = Np;
+    g.k = k;
+    const unsigned blocks = static_cast<unsigned>((sp / BM) * ((2 * Np) / BN));
+    for (int64_t t = 0; t < nsteps; ++t) {
+        g.step = step0 + t + 1;
+        g.Bop = BA;
+        dense_rk4_gemm<0><<<blocks, THREADS, kSmemBytes, stream>>>(g);
+        g.Bop = BB;
+        dense_rk4_gemm<1><<<blocks, THREADS, kSmemBytes, stream>>>(g);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_pack(const double *X, const double *V0, double *BA, double *Vp,
+                              int64_t s, int64_t N, int64_t sp, int64_t Np, double h,
+                              cudaStream_t stream)
+{
+    const int64_t total = sp * Np;
+    pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(X, V0, BA, Vp, s,
+                                                                                 N, sp, Np, h);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_unpack(const double *BA, const double *Vp, double *X, double *V,
+                                int64_t s, int64_t N, int64_t Np, cudaStream_t stream)
+{
+    const int64_t total = s * N;
+    unpack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(BA, Vp, X, V,
+                                                                                   s, N, Np);
+    return cudaGetLastError();
+}
+
+}  // namespace osc

@@ -131,6 +131,40 @@ __global__ void fp64_peak_kernel(int64_t iters, int mode, double *sink)
         sink[threadIdx.x] = s;
 }
 
+// FP64 tensor-core issue rate: 8 independent DMMA.8x8x4 accumulators per
+// warp (mma.sync m8n8k4 f64; tcgen05 has no f64 kind on sm_100a).  mode 3
+// interleaves 8 DFMA chains to see whether DMMA and DFMA share a pipe.
+__global__ void dmma_peak_kernel(int64_t iters, int mode, double *sink)
+{
+    double acc[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        acc[j][0] = acc[j][1] = 0.0;
+    const double a = 1.0 + 1e-3 * threadIdx.x, b = 0.5;
+    double f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        f[j] = 1.0 + j;
+    for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[j][0]), "+d"(acc[j][1])
+                         : "d"(a), "d"(b));
+        if (mode == 3) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                f[j] = __fma_rn(f[j], 0.999999, 1e-7);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        s += acc[j][0] + acc[j][1] + f[j];
+    if (s == 12345.678)
+        sink[threadIdx.x] = s;
+}
+
 }  // namespace
 
 cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lanes_ops,
@@ -140,6 +174,13 @@ cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lan
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int blocks = sms * 4, threads = 512;
+    if (mode >= 2) {
+        // returned count = flops: 512 per DMMA.8x8x4 per warp (+ 2 per DFMA lane in mode 3)
+        dmma_peak_kernel<<<blocks, threads, 0, stream>>>(iters, mode, sink);
+        const int64_t warps = int64_t(blocks) * threads / 32;
+        *lanes_ops = warps * iters * 8 * 512 + (mode == 3 ? int64_t(blocks) * threads * iters * 16 : 0);
+        return cudaGetLastError();
+    }
     fp64_peak_kernel<<<blocks, threads, 0, stream>>>(iters, mode, sink);
     *lanes_ops = int64_t(blocks) * threads * iters * 8;
     return cudaGetLastError();

@@ -43,4 +43,18 @@ cudaError_t launch_check_division(int64_t n, uint64_t seed, int mode,
 cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lanes_ops,
                              cudaStream_t stream);
 
+// K5 dense path (k_dense.cu): padded sizes s -> multiple of 128, N -> of 32.
+int64_t dense_pad_s(int64_t s);
+int64_t dense_pad_n(int64_t n);
+cudaError_t launch_rowscale(const double *K, const double *m, double *A, int64_t s, int64_t sp,
+                            cudaStream_t stream);
+cudaError_t launch_dense_pack(const double *X, const double *V0, double *BA, double *Vp,
+                              int64_t s, int64_t N, int64_t sp, int64_t Np, double h,
+                              cudaStream_t stream);
+cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *Vp, double *SX,
+                               double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
+                               StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream);
+cudaError_t launch_dense_unpack(const double *BA, const double *Vp, double *X, double *V,
+                                int64_t s, int64_t N, int64_t Np, cudaStream_t stream);
+
 }  // namespace osc

@@ -27,16 +27,29 @@
 #include "osc_device.cuh"
 #include "osc_kernels.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace osc {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
-constexpr int APAD = 4, BPAD = 8;  // doubles of row padding (bank-conflict-free fragments)
-constexpr int AS = BK + APAD;      // A smem row stride
-constexpr int BS = BN + BPAD;      // B smem row stride
-constexpr int THREADS = 256;
-constexpr size_t kStageDoubles = size_t(BM) * AS + size_t(BK) * BS;
-constexpr size_t kSmemBytes = STAGES * kStageDoubles * sizeof(double);
+constexpr int BM = 128, BN = 64;
+// Row padding so that each half-warp phase of a 64-bit fragment load hits 32
+// distinct banks: A rows (8 rows x 4 k) and B rows (4 k x 8 cols) must start
+// 8 banks apart, i.e. strides of 4 (mod 16) doubles.
+constexpr int APAD = 4, BPAD = 4;
+constexpr int BS = BN + BPAD;  // B smem row stride
+
+// Pipeline shape: BK doubles of K per shared-memory slab, STAGES slabs in flight.
+template <int BK_, int STAGES_>
+struct Pipe {
+    static constexpr int BK = BK_, STAGES = STAGES_;
+    static constexpr int AS = BK + APAD;  // A smem row stride
+    static constexpr size_t kStageDoubles = size_t(BM) * AS + size_t(BK) * BS;
+    static constexpr size_t kPipeBytes = STAGES * kStageDoubles * sizeof(double);
+    static constexpr size_t kEpiBytes = size_t(BM) * (BN + 1) * sizeof(double);
+    static constexpr size_t kSmemBytes = kPipeBytes > kEpiBytes ? kPipeBytes : kEpiBytes;
+};
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
@@ -68,6 +81,7 @@ struct DenseArgs {
 };
 
 // Stage one BK-slab of A (rows m0..m0+BM) and of Bop (cols n0..n0+BN).
+template <int THREADS, int BK, int AS>
 __device__ __forceinline__ void load_stage(const DenseArgs &g, double *sA, double *sB,
                                            int64_t m0, int64_t n0, int64_t k0)
 {
@@ -89,12 +103,21 @@ __device__ __forceinline__ void load_stage(const DenseArgs &g, double *sA, doubl
     }
 }
 
-template <int kStage>
-__global__ void __launch_bounds__(THREADS, 1) dense_rk4_gemm(DenseArgs g)
+// KG k-groups of 8 warps: group kg issues the k4-steps kk/4 = kg (mod KG) of
+// every BK slab into its own accumulators; the groups' partial tiles are
+// summed in a fixed order (group 0 + group 1) before the epilogue, so results
+// are deterministic.  KG = 2 doubles the warps per scheduler without
+// changing the tile count (wave efficiency).
+template <int kStage, int KG, class P>
+__global__ void __launch_bounds__(256 * KG, 1) dense_rk4_gemm(DenseArgs g)
 {
+    constexpr int THREADS = 256 * KG;
+    constexpr int BK = P::BK, STAGES = P::STAGES, AS = P::AS;
+    constexpr size_t kStageDoubles = P::kStageDoubles;
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps of 32 x 32
+    const int kg = warp >> 3, w8 = warp & 7;
+    const int wm = w8 & 3, wn = w8 >> 2;  // 4 x 2 warps of 32 x 32 per k-group
     const int64_t ntn = (2 * g.N) / BN;
     const int64_t m0 = static_cast<int64_t>(blockIdx.x / ntn) * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x % ntn) * BN;
@@ -110,8 +133,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_rk4_gemm(DenseArgs g)
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
         if (st < KT)
-            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS, m0, n0,
-                       st * BK);
+            load_stage<THREADS, BK, AS>(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS,
+                                m0, n0, st * BK);
         cp_commit();
     }
     const int ar = lane >> 2, ac = lane & 3;  // fragment coordinates
@@ -121,14 +144,16 @@ __global__ void __launch_bounds__(THREADS, 1) dense_rk4_gemm(DenseArgs g)
         const int64_t nk = kt + STAGES - 1;
         if (nk < KT) {
             const int st = nk % STAGES;
-            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS, m0, n0,
-                       nk * BK);
+            load_stage<THREADS, BK, AS>(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS,
+                                m0, n0, nk * BK);
         }
         cp_commit();
         const double *sA = smem + (kt % STAGES) * kStageDoubles;
         const double *sB = sA + BM * AS;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
+            if ((kk / 4) % KG != kg)
+                continue;
             double af[4], bf[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -150,15 +175,35 @@ __global__ void __launch_bounds__(THREADS, 1) dense_rk4_gemm(DenseArgs g)
     // thread sees both halves (stage j and j+1) of its trajectories.
     double *sC = smem;  // BM x (BN + 1)
     constexpr int CS = BN + 1;
+    if (KG == 2 && kg == 1) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int r = wm * 32 + i * 8 + ar;
-            const int c = wn * 32 + j * 8 + 2 * ac;
-            sC[r * CS + c] = acc[i][j][0];
-            sC[r * CS + c + 1] = acc[i][j][1];
-        }
+            for (int j = 0; j < 4; ++j) {
+                const int r = wm * 32 + i * 8 + ar;
+                const int c = wn * 32 + j * 8 + 2 * ac;
+                sC[r * CS + c] = acc[i][j][0];
+                sC[r * CS + c + 1] = acc[i][j][1];
+            }
+    }
+    if (KG == 2)
+        __syncthreads();
+    if (kg == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int r = wm * 32 + i * 8 + ar;
+                const int c = wn * 32 + j * 8 + 2 * ac;
+                if (KG == 2) {
+                    sC[r * CS + c] = add(acc[i][j][0], sC[r * CS + c]);
+                    sC[r * CS + c + 1] = add(acc[i][j][1], sC[r * CS + c + 1]);
+                } else {
+                    sC[r * CS + c] = acc[i][j][0];
+                    sC[r * CS + c + 1] = acc[i][j][1];
+                }
+            }
+    }
     __syncthreads();
 
     const int64_t cb = n0 / BN;  // trajectory block
@@ -258,10 +303,16 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
                                double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
                                StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream)
 {
-    cudaFuncSetAttribute(dense_rk4_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kSmemBytes));
-    cudaFuncSetAttribute(dense_rk4_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kSmemBytes));
+    // Launch shape; OSC_DENSE="KG,BK,STAGES" overrides it (benchmarking only).
+    int kgroups = 2, bk = 32, stages = 3;
+    if (const char *e = std::getenv("OSC_DENSE")) {
+        int a = 0, b = 0, c = 0;
+        if (std::sscanf(e, "%d,%d,%d", &a, &b, &c) == 3) {
+            kgroups = a;
+            bk = b;
+            stages = c;
+        }
+    }
     DenseArgs g{};
     g.A = A;
     g.BA = BA;
@@ -274,14 +325,33 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
     g.N = Np;
     g.k = k;
     const unsigned blocks = static_cast<unsigned>((sp / BM) * ((2 * Np) / BN));
-    for (int64_t t = 0; t < nsteps; ++t) {
-        g.step = step0 + t + 1;
-        g.Bop = BA;
-        dense_rk4_gemm<0><<<blocks, THREADS, kSmemBytes, stream>>>(g);
-        g.Bop = BB;
-        dense_rk4_gemm<1><<<blocks, THREADS, kSmemBytes, stream>>>(g);
-    }
-    return cudaGetLastError();
+    cudaError_t err = cudaSuccess;
+    auto run = [&](auto stage0, auto stage1, int threads, size_t smem) {
+        cudaFuncSetAttribute(stage0, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        cudaFuncSetAttribute(stage1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        for (int64_t t = 0; t < nsteps; ++t) {
+            g.step = step0 + t + 1;
+            g.Bop = BA;
+            stage0<<<blocks, threads, smem, stream>>>(g);
+            g.Bop = BB;
+            stage1<<<blocks, threads, smem, stream>>>(g);
+        }
+        err = cudaGetLastError();
+    };
+    using P16x4 = Pipe<16, 4>;
+    using P32x3 = Pipe<32, 3>;
+    using P32x4 = Pipe<32, 4>;
+    if (kgroups == 1 && bk == 16)
+        run(dense_rk4_gemm<0, 1, P16x4>, dense_rk4_gemm<1, 1, P16x4>, 256, P16x4::kSmemBytes);
+    else if (bk == 16)
+        run(dense_rk4_gemm<0, 2, P16x4>, dense_rk4_gemm<1, 2, P16x4>, 512, P16x4::kSmemBytes);
+    else if (stages == 4)
+        run(dense_rk4_gemm<0, 2, P32x4>, dense_rk4_gemm<1, 2, P32x4>, 512, P32x4::kSmemBytes);
+    else
+        run(dense_rk4_gemm<0, 2, P32x3>, dense_rk4_gemm<1, 2, P32x3>, 512, P32x3::kSmemBytes);
+    return err;
 }
 
 cudaError_t launch_dense_pack(const double *X, const double *V0, double *BA, double *Vp,

@@ -13,17 +13,14 @@
 // [s x s] x [s x 2N]:  [k1|k2] = -A [x|y2]  and  [k3|k4] = -A [y3|y4],
 // each with the RK4 elementwise work fused into its epilogue.
 //
-// Operand layout: BA / BB are [s][2N] with columns blocked by 32 trajectories:
-// block cb holds columns (x of trajectories 32cb..32cb+31 | y2 of the same),
-// so one 64-column CTA tile owns both halves of its 32 trajectories and the
-// epilogue is local.  x itself lives in BA's first halves.
+// Operand layout: BA / BB are [s][2N] with columns blocked by TB = 16
+// trajectories: block cb holds columns (x of trajectories 16cb..16cb+15 | y2
+// of the same), so one 32-column CTA tile owns both halves of its 16
+// trajectories and the epilogue is local.  x itself lives in BA's first
+// halves.
 //
 // GEMM: FP64 tensor cores through mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4;
-// tcgen05 has no f64 kind on sm_100a -- ptxas rejects kind::f64).  CTA tile
-// 128 x 64, 8 warps of 32 x 32 (16 DMMA accumulators each), BK = 16,
-// 4-stage cp.async pipeline, padded shared-memory rows (conflict-free
-// fragment loads).  128x64 tiles give 1024 CTAs per GEMM at s=4096, N=1024:
-// 6.92 waves of 148 -> 98.8% wave efficiency.
+// tcgen05 has no f64 kind on sm_100a -- ptxas rejects kind::f64).
 #include "osc_device.cuh"
 #include "osc_kernels.h"
 
@@ -33,23 +30,28 @@
 namespace osc {
 namespace {
 
-constexpr int BM = 128, BN = 64;
-// Row padding so that each half-warp phase of a 64-bit fragment load hits 32
-// distinct banks: A rows (8 rows x 4 k) and B rows (4 k x 8 cols) must start
-// 8 banks apart, i.e. strides of 4 (mod 16) doubles.
-constexpr int APAD = 4, BPAD = 4;
-constexpr int BS = BN + BPAD;  // B smem row stride
+// CTA tile 64 x 32 (16 trajectories x both halves), 4 warps of 32 x 16 (8
+// DMMA accumulators each), BK = 16, 4-stage cp.async pipeline, 48 KB of
+// shared memory -> 4 CTAs (16 warps) per SM and 4096 CTAs per GEMM at
+// s = 4096, N = 1024: 6.92 waves of 592, 98.8% wave efficiency.  (The same
+// tiling cuBLAS picks for this shape, cutlass d884gemm_64x32_16x4.)
+constexpr int BM = 64, BN = 32, BK = 16, STAGES = 4, THREADS = 128;
+constexpr int TB = BN / 2;  // trajectories per operand block
+constexpr size_t kStageDoubles = size_t(BM) * BK + size_t(BK) * BN;
+constexpr size_t kSmemBytes = STAGES * kStageDoubles * sizeof(double);
+static_assert(size_t(BM) * (BN + 1) <= STAGES * kStageDoubles, "epilogue staging fits");
 
-// Pipeline shape: BK doubles of K per shared-memory slab, STAGES slabs in flight.
-template <int BK_, int STAGES_>
-struct Pipe {
-    static constexpr int BK = BK_, STAGES = STAGES_;
-    static constexpr int AS = BK + APAD;  // A smem row stride
-    static constexpr size_t kStageDoubles = size_t(BM) * AS + size_t(BK) * BS;
-    static constexpr size_t kPipeBytes = STAGES * kStageDoubles * sizeof(double);
-    static constexpr size_t kEpiBytes = size_t(BM) * (BN + 1) * sizeof(double);
-    static constexpr size_t kSmemBytes = kPipeBytes > kEpiBytes ? kPipeBytes : kEpiBytes;
-};
+// XOR swizzle of 16-byte chunks so that each half-warp phase of a 64-bit
+// fragment load (4 rows x 4 consecutive doubles) hits 32 distinct banks
+// without padding: chunk q of row r lives at q ^ 2*(r % 4).
+__device__ __forceinline__ int swz_a(int r, int k)  // A tile [BM][BK]
+{
+    return r * BK + ((((k >> 1) ^ ((r & 3) << 1))) << 1) + (k & 1);
+}
+__device__ __forceinline__ int swz_b(int k, int n)  // B tile [BK][BN]
+{
+    return k * BN + ((((n >> 1) ^ ((k & 3) << 1))) << 1) + (n & 1);
+}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
@@ -70,71 +72,59 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
 struct DenseArgs {
     const double *A;   // [s][s] row-major, A = M^-1 K
     const double *Bop; // [s][2N] blocked operand of this GEMM
-    double *BA;        // [s][2N]  (x | y2) blocks
+    double *BA;        // [s][2N]  (x | y2) blocks of TB trajectories
     double *BB;        // [s][2N]  (y3 | y4) blocks
     double *V;         // [s][N]
     double *SX, *SV;   // [s][N] partial combination sums
     int64_t *first_bad;
-    int64_t s, N;      // padded sizes: s % BM == 0, N % 32 == 0
+    int64_t s, N;      // padded sizes: s % 64 == 0, N % TB == 0
     StepConsts k;
     int64_t step;      // 1-based step index (divergence tag)
 };
 
 // Stage one BK-slab of A (rows m0..m0+BM) and of Bop (cols n0..n0+BN).
-template <int THREADS, int BK, int AS>
 __device__ __forceinline__ void load_stage(const DenseArgs &g, double *sA, double *sB,
                                            int64_t m0, int64_t n0, int64_t k0)
 {
     const int tid = threadIdx.x;
     const int64_t ld2 = 2 * g.N;
-    // A: BM x BK doubles = BM*BK/2 chunks of 16 B
 #pragma unroll
-    for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {
+    for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {  // A: BM rows x BK/2 chunks
         const int c = tid + i * THREADS;
         const int r = c / (BK / 2), q = c % (BK / 2);
-        cp_async16(sA + r * AS + 2 * q, g.A + (m0 + r) * g.s + k0 + 2 * q);
+        cp_async16(sA + swz_a(r, 2 * q), g.A + (m0 + r) * g.s + k0 + 2 * q);
     }
-    // B: BK x BN doubles
 #pragma unroll
-    for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {
+    for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {  // B: BK rows x BN/2 chunks
         const int c = tid + i * THREADS;
         const int r = c / (BN / 2), q = c % (BN / 2);
-        cp_async16(sB + r * BS + 2 * q, g.Bop + (k0 + r) * ld2 + n0 + 2 * q);
+        cp_async16(sB + swz_b(r, 2 * q), g.Bop + (k0 + r) * ld2 + n0 + 2 * q);
     }
 }
 
-// KG k-groups of 8 warps: group kg issues the k4-steps kk/4 = kg (mod KG) of
-// every BK slab into its own accumulators; the groups' partial tiles are
-// summed in a fixed order (group 0 + group 1) before the epilogue, so results
-// are deterministic.  KG = 2 doubles the warps per scheduler without
-// changing the tile count (wave efficiency).
-template <int kStage, int KG, class P>
-__global__ void __launch_bounds__(256 * KG, 1) dense_rk4_gemm(DenseArgs g)
+template <int kStage>
+__global__ void __launch_bounds__(THREADS, 4) dense_rk4_gemm(DenseArgs g)
 {
-    constexpr int THREADS = 256 * KG;
-    constexpr int BK = P::BK, STAGES = P::STAGES, AS = P::AS;
-    constexpr size_t kStageDoubles = P::kStageDoubles;
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int kg = warp >> 3, w8 = warp & 7;
-    const int wm = w8 & 3, wn = w8 >> 2;  // 4 x 2 warps of 32 x 32 per k-group
+    const int wm = warp & 1, wn = warp >> 1;  // 2 x 2 warps of 32 x 16
     const int64_t ntn = (2 * g.N) / BN;
     const int64_t m0 = static_cast<int64_t>(blockIdx.x / ntn) * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x % ntn) * BN;
     const int64_t KT = g.s / BK;
 
-    double acc[4][4][2];
+    double acc[4][2][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 2; ++j)
             acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
         if (st < KT)
-            load_stage<THREADS, BK, AS>(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS,
-                                m0, n0, st * BK);
+            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * BK, m0, n0,
+                       st * BK);
         cp_commit();
     }
     const int ar = lane >> 2, ac = lane & 3;  // fragment coordinates
@@ -144,79 +134,57 @@ __global__ void __launch_bounds__(256 * KG, 1) dense_rk4_gemm(DenseArgs g)
         const int64_t nk = kt + STAGES - 1;
         if (nk < KT) {
             const int st = nk % STAGES;
-            load_stage<THREADS, BK, AS>(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * AS,
-                                m0, n0, nk * BK);
+            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * BK, m0, n0,
+                       nk * BK);
         }
         cp_commit();
         const double *sA = smem + (kt % STAGES) * kStageDoubles;
-        const double *sB = sA + BM * AS;
+        const double *sB = sA + BM * BK;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            if ((kk / 4) % KG != kg)
-                continue;
-            double af[4], bf[4];
+            double af[4], bf[2];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                af[i] = sA[(wm * 32 + i * 8 + ar) * AS + kk + ac];
+                af[i] = sA[swz_a(wm * 32 + i * 8 + ar, kk + ac)];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                bf[j] = sB[(kk + ac) * BS + wn * 32 + j * 8 + ar];
+            for (int j = 0; j < 2; ++j)
+                bf[j] = sB[swz_b(kk + ac, wn * 16 + j * 8 + ar)];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < 2; ++j)
                     dmma(acc[i][j], af[i], bf[j]);
         }
     }
     cp_wait<0>();
     __syncthreads();
 
-    // Stage the 128 x 64 accumulator tile through shared memory so each
+    // Stage the 64 x 32 accumulator tile through shared memory so each
     // thread sees both halves (stage j and j+1) of its trajectories.
-    double *sC = smem;  // BM x (BN + 1)
+    double *sC = smem;
     constexpr int CS = BN + 1;
-    if (KG == 2 && kg == 1) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int r = wm * 32 + i * 8 + ar;
-                const int c = wn * 32 + j * 8 + 2 * ac;
-                sC[r * CS + c] = acc[i][j][0];
-                sC[r * CS + c + 1] = acc[i][j][1];
-            }
-    }
-    if (KG == 2)
-        __syncthreads();
-    if (kg == 0) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int r = wm * 32 + i * 8 + ar;
-                const int c = wn * 32 + j * 8 + 2 * ac;
-                if (KG == 2) {
-                    sC[r * CS + c] = add(acc[i][j][0], sC[r * CS + c]);
-                    sC[r * CS + c + 1] = add(acc[i][j][1], sC[r * CS + c + 1]);
-                } else {
-                    sC[r * CS + c] = acc[i][j][0];
-                    sC[r * CS + c + 1] = acc[i][j][1];
-                }
-            }
-    }
+        for (int j = 0; j < 2; ++j) {
+            const int r = wm * 32 + i * 8 + ar;
+            const int c = wn * 16 + j * 8 + 2 * ac;
+            sC[r * CS + c] = acc[i][j][0];
+            sC[r * CS + c + 1] = acc[i][j][1];
+        }
     __syncthreads();
 
     const int64_t cb = n0 / BN;  // trajectory block
     const double h = g.k.half_dt, dt = g.k.dt, dt6 = g.k.dt6;
     const int64_t ld2 = 2 * g.N;
     bool bad = false;
-    for (int e = tid; e < BM * 32; e += THREADS) {
-        const int r = e >> 5, c = e & 31;
+    for (int e = tid; e < BM * TB; e += THREADS) {
+        const int r = e / TB, c = e % TB;
         const int64_t gr = m0 + r;
-        const int64_t n = cb * 32 + c;               // trajectory
+        const int64_t n = cb * TB + c;               // trajectory
         const int64_t ix = gr * ld2 + cb * BN + c;   // its first-half column
         const double p = -sC[r * CS + c];            // k1 (stage 0) or k3 (stage 1)
-        const double q = -sC[r * CS + c + 32];       // k2 or k4
+        const double q = -sC[r * CS + c + TB];       // k2 or k4
         const double x = g.BA[ix];
         const double v = g.V[gr * g.N + n];
         if constexpr (kStage == 0) {
@@ -224,7 +192,7 @@ __global__ void __launch_bounds__(256 * KG, 1) dense_rk4_gemm(DenseArgs g)
             const double y2v = add(v, mul(h, p));
             const double y3v = add(v, mul(h, q));
             g.BB[ix] = add(x, mul(h, y2v));
-            g.BB[ix + 32] = add(x, mul(dt, y3v));
+            g.BB[ix + TB] = add(x, mul(dt, y3v));
             g.SX[gr * g.N + n] = add(add(v, mul(2.0, y2v)), mul(2.0, y3v));
             g.SV[gr * g.N + n] = add(p, mul(2.0, q));
         } else {
@@ -236,7 +204,7 @@ __global__ void __launch_bounds__(256 * KG, 1) dense_rk4_gemm(DenseArgs g)
             const double vn = add(v, mul(dt6, sv));
             g.BA[ix] = xn;
             g.V[gr * g.N + n] = vn;
-            g.BA[ix + 32] = add(xn, mul(h, vn));  // y2p of the next step
+            g.BA[ix + TB] = add(xn, mul(h, vn));  // y2p of the next step
             bad |= !(finite(xn) & finite(vn));
         }
     }
@@ -266,9 +234,9 @@ __global__ void pack_kernel(const double *__restrict__ X, const double *__restri
     const int64_t r = i / Np, n = i % Np;
     const bool in = r < s && n < N;
     const double x = in ? X[r * N + n] : 0.0, v = in ? V0[r * N + n] : 0.0;
-    const int64_t ix = r * 2 * Np + (n / 32) * 64 + (n % 32);
+    const int64_t ix = r * 2 * Np + (n / TB) * BN + (n % TB);
     BA[ix] = x;
-    BA[ix + 32] = add(x, mul(h, v));
+    BA[ix + TB] = add(x, mul(h, v));
     Vp[r * Np + n] = v;
 }
 
@@ -280,14 +248,14 @@ __global__ void unpack_kernel(const double *__restrict__ BA, const double *__res
     if (i >= s * N)
         return;
     const int64_t r = i / N, n = i % N;
-    X[i] = BA[r * 2 * Np + (n / 32) * 64 + (n % 32)];
+    X[i] = BA[r * 2 * Np + (n / TB) * BN + (n % TB)];
     V[i] = Vp[r * Np + n];
 }
 
 }  // namespace
 
-int64_t dense_pad_s(int64_t s) { return (s + BM - 1) / BM * BM; }
-int64_t dense_pad_n(int64_t n) { return (n + 31) / 32 * 32; }
+int64_t dense_pad_s(int64_t s) { return (s + BM - 1) / BM * BM; }  // also a multiple of BK
+int64_t dense_pad_n(int64_t n) { return (n + TB - 1) / TB * TB; }
 
 cudaError_t launch_rowscale(const double *K, const double *m, double *A, int64_t s, int64_t sp,
                             cudaStream_t stream)
@@ -303,16 +271,6 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
                                double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
                                StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream)
 {
-    // Launch shape; OSC_DENSE="KG,BK,STAGES" overrides it (benchmarking only).
-    int kgroups = 2, bk = 32, stages = 3;
-    if (const char *e = std::getenv("OSC_DENSE")) {
-        int a = 0, b = 0, c = 0;
-        if (std::sscanf(e, "%d,%d,%d", &a, &b, &c) == 3) {
-            kgroups = a;
-            bk = b;
-            stages = c;
-        }
-    }
     DenseArgs g{};
     g.A = A;
     g.BA = BA;
@@ -324,34 +282,19 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
     g.s = sp;
     g.N = Np;
     g.k = k;
+    cudaFuncSetAttribute(dense_rk4_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(dense_rk4_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
     const unsigned blocks = static_cast<unsigned>((sp / BM) * ((2 * Np) / BN));
-    cudaError_t err = cudaSuccess;
-    auto run = [&](auto stage0, auto stage1, int threads, size_t smem) {
-        cudaFuncSetAttribute(stage0, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        cudaFuncSetAttribute(stage1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        for (int64_t t = 0; t < nsteps; ++t) {
-            g.step = step0 + t + 1;
-            g.Bop = BA;
-            stage0<<<blocks, threads, smem, stream>>>(g);
-            g.Bop = BB;
-            stage1<<<blocks, threads, smem, stream>>>(g);
-        }
-        err = cudaGetLastError();
-    };
-    using P16x4 = Pipe<16, 4>;
-    using P32x3 = Pipe<32, 3>;
-    using P32x4 = Pipe<32, 4>;
-    if (kgroups == 1 && bk == 16)
-        run(dense_rk4_gemm<0, 1, P16x4>, dense_rk4_gemm<1, 1, P16x4>, 256, P16x4::kSmemBytes);
-    else if (bk == 16)
-        run(dense_rk4_gemm<0, 2, P16x4>, dense_rk4_gemm<1, 2, P16x4>, 512, P16x4::kSmemBytes);
-    else if (stages == 4)
-        run(dense_rk4_gemm<0, 2, P32x4>, dense_rk4_gemm<1, 2, P32x4>, 512, P32x4::kSmemBytes);
-    else
-        run(dense_rk4_gemm<0, 2, P32x3>, dense_rk4_gemm<1, 2, P32x3>, 512, P32x3::kSmemBytes);
-    return err;
+    for (int64_t t = 0; t < nsteps; ++t) {
+        g.step = step0 + t + 1;
+        g.Bop = BA;
+        dense_rk4_gemm<0><<<blocks, THREADS, kSmemBytes, stream>>>(g);
+        g.Bop = BB;
+        dense_rk4_gemm<1><<<blocks, THREADS, kSmemBytes, stream>>>(g);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_dense_pack(const double *X, const double *V0, double *BA, double *Vp,

@@ -56,8 +56,8 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     double yp1 = add(s.x1, mul(k.half_dt, s.v1));
     // k2 at the midpoint; y2v doubles as the k2 position slope.
     accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
-    sx0 = add(sx0, mul(2.0, yv0));
-    sx1 = add(sx1, mul(2.0, yv1));
+    sx0 = add_twice_checked<kExact>(sx0, yv0, ok);
+    sx1 = add_twice_checked<kExact>(sx1, yv1, ok);
     sv0 = add_twice<kExact>(sv0, a0);
     sv1 = add_twice<kExact>(sv1, a1);
     yp0 = add(s.x0, mul(k.half_dt, yv0));
@@ -66,8 +66,8 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     yv1 = add(s.v1, mul(k.half_dt, a1));
     // k3 at the refined midpoint.
     accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
-    sx0 = add(sx0, mul(2.0, yv0));
-    sx1 = add(sx1, mul(2.0, yv1));
+    sx0 = add_twice_checked<kExact>(sx0, yv0, ok);
+    sx1 = add_twice_checked<kExact>(sx1, yv1, ok);
     sv0 = add_twice<kExact>(sv0, a0);
     sv1 = add_twice<kExact>(sv1, a1);
     yp0 = add(s.x0, mul(k.dt, yv0));
@@ -233,6 +233,13 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
     // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
     // overrides it for benchmarking (read-only process state).
     int ns = kBatch2NS, threads = kBatch2Threads;
+    // Too few systems to fill the GPU: one system per thread keeps each
+    // thread's serial recurrence short (C1 is a single latency-bound system).
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (B < int64_t(sms) * 1024)
+        ns = 1;
     if (const char *e = std::getenv("OSC_B2")) {
         int a = 0, b = 0;
         if (std::sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && b >= 32 &&

@@ -107,7 +107,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
     accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k2
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        sx[j] = add(sx[j], mul(2.0, yv[j]));
+        sx[j] = add_twice_checked<kExact>(sx[j], yv[j], ok);
         sv[j] = add_twice<kExact>(sv[j], a[j]);
         yp[j] = add(x[j], mul(k.half_dt, yv[j]));
         yv[j] = add(v[j], mul(k.half_dt, a[j]));
@@ -115,7 +115,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
     accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k3
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        sx[j] = add(sx[j], mul(2.0, yv[j]));
+        sx[j] = add_twice_checked<kExact>(sx[j], yv[j], ok);
         sv[j] = add_twice<kExact>(sv[j], a[j]);
         yp[j] = add(x[j], mul(k.dt, yv[j]));
         yv[j] = add(v[j], mul(k.dt, a[j]));
@@ -160,6 +160,8 @@ __device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v
 template <int K>
 constexpr int max_threads() { return K <= 1 ? 1024 : K == 2 ? 512 : 256; }
 
+// NT: max threads per CTA, MINB: CTAs per SM the register allocation must
+// allow (__launch_bounds__).
 template <int K, bool kPad>
 __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 {
@@ -245,11 +247,12 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
         return cudaErrorInvalidConfiguration;
     const int64_t blocks = g.tiles * g.nbuf;
     const int64_t TILE = int64_t(threads) * K;
+    const unsigned nb = static_cast<unsigned>(blocks);
     // Padding is needed only when a tile is longer than the whole buffer.
     if (TILE > g.n)
-        chain_rk4_kernel<K, true><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(g);
+        chain_rk4_kernel<K, true><<<nb, threads, 0, stream>>>(g);
     else
-        chain_rk4_kernel<K, false><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(g);
+        chain_rk4_kernel<K, false><<<nb, threads, 0, stream>>>(g);
     return cudaGetLastError();
 }
 

@@ -146,7 +146,7 @@ class Workload:
                          "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
         elif name == "C3":
             arrays = workloads.c3()
-            T = halo or 16
+            T = halo or 32
             self.kernel = "chain_rk4_kernel<8>"
             self.launches = -(-p.nsteps // T)
             self.world = world

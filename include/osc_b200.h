@@ -63,7 +63,7 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
  * (spring i joins cell i to cell i-1, spring 0 to the wall, last cell free;
  * oscillator.py:3-5, 152-164).  Chains up to 2048 cells run one CTA per chain
  * for the whole run; longer chains use temporally blocked tiles of
- * halo_steps steps per launch (0 = default 16).
+ * halo_steps steps per launch (0 = default 32).
  * Replaces integrate() (oscillator.py:234-263).
  * xs/vs: [1 + nsteps/stride][B][s].  first_bad: [B]. */
 int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B,

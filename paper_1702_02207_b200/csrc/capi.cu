@@ -61,11 +61,12 @@ osc::StepConsts consts(double dt)
 
 constexpr int64_t kWholeChainMax = 2048;  // 256 threads x 8 cells
 constexpr int64_t kWholeChainSteps = 512; // steps per launch in whole-chain mode
-// Tiled shape, measured on B200 for s = 2^24 (profiles/r01): 8 cells x 128
-// threads with 16-step halos beat 8x256 (T=16,32,64) and 4x256.
-constexpr int kTileK = 8, kTileThreads = 128;
+// Tiled shape, measured on B200 for s = 2^24 (profiles/r01): with the
+// persistent prefetching kernel, 8 cells x 256 threads and 32-step halos
+// (2.57e11 DOF-steps/s) beat 8x128 (T=16: 2.36e11, T=32: 2.44e11).
+constexpr int kTileK = 8, kTileThreads = 256;
 constexpr int64_t kTile = int64_t(kTileK) * kTileThreads;
-constexpr int64_t kDefaultHaloSteps = 16;
+constexpr int64_t kDefaultHaloSteps = 32;
 
 void pick_whole(int64_t s, int &K, int &threads)
 {

@@ -27,6 +27,9 @@
 #include "osc_device.cuh"
 #include "osc_kernels.h"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace osc {
 namespace {
 
@@ -160,17 +163,21 @@ __device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v
 template <int K>
 constexpr int max_threads() { return K <= 1 ? 1024 : K == 2 ? 512 : 256; }
 
-// NT: max threads per CTA, MINB: CTAs per SM the register allocation must
-// allow (__launch_bounds__).
 template <int K, bool kPad>
 __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 {
     __shared__ double s_lo[2][kMaxWarps];
     __shared__ double s_hi[2][kMaxWarps];
 
+    __shared__ int s_skip;
     const int64_t buf_id = blockIdx.x / g.tiles;
     const int64_t tile = blockIdx.x % g.tiles;
-    if (g.first_bad[buf_id] != 0)
+    // One read, broadcast: another CTA may record a divergence at any time,
+    // and the exit must be uniform across this CTA's barriers.
+    if (threadIdx.x == 0)
+        s_skip = g.first_bad[buf_id] != 0;
+    __syncthreads();
+    if (s_skip)
         return;  // already diverged: state is unspecified, as integrate raised
 
     const int64_t TILE = static_cast<int64_t>(blockDim.x) * K;
@@ -240,6 +247,200 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent tiled form (K3 for long chains): each CTA walks a strided list
+// of tiles and prefetches the NEXT tile's m, C, x, v into a second shared-
+// memory buffer with bulk async copies (cp.async.bulk, TMA engine, mbarrier
+// completion) while it integrates the current one, so the per-tile HBM load
+// latency overlaps compute.  The tile input stays in shared memory until the
+// tile is finished, which is what the exact replay reloads from.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p)
+{
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct TileGeom {
+    int64_t buf_id, base, L, own_start, own_end;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(const SegArgs &g, int64_t it, int64_t TILE)
+{
+    TileGeom tg;
+    tg.buf_id = it / g.tiles;
+    const int64_t tile = it % g.tiles;
+    tg.own_start = g.own_lo + tile * g.W;
+    tg.own_end = min(tg.own_start + g.W, g.own_hi);
+    tg.L = max(static_cast<int64_t>(0), tg.own_start - g.H);
+    if (tg.L + TILE > g.n)
+        tg.L = g.n - TILE;
+    tg.base = tg.buf_id * g.n;
+    return tg;
+}
+
+template <int K, int NT>
+__device__ __forceinline__ void issue_tile(const SegArgs &g, int64_t it, double *dst,
+                                           uint64_t *bar)
+{
+    constexpr int64_t TILE = int64_t(NT) * K;
+    constexpr unsigned bytes = TILE * sizeof(double);
+    const TileGeom tg = tile_geom(g, it, TILE);
+    const int64_t o = tg.base + tg.L;
+    mbar_expect_tx(bar, 4 * bytes);
+    bulk_g2s(dst, g.m + o, bytes, bar);
+    bulk_g2s(dst + TILE, g.C + o, bytes, bar);
+    bulk_g2s(dst + 2 * TILE, g.xin + o, bytes, bar);
+    bulk_g2s(dst + 3 * TILE, g.vin + o, bytes, bar);
+}
+
+template <int K, int NT>
+__global__ void __launch_bounds__(NT) chain_tiles_persistent(SegArgs g)
+{
+    constexpr int64_t TILE = int64_t(NT) * K;
+    extern __shared__ __align__(128) double tbuf[];  // 2 x [m | C | x | v] x TILE
+    __shared__ double s_lo[2][kMaxWarps];
+    __shared__ double s_hi[2][kMaxWarps];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ int s_skip;
+
+    const int64_t ntiles = g.tiles * g.nbuf;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b < 2; ++b) {
+            const int64_t it = blockIdx.x + int64_t(b) * gridDim.x;
+            if (it < ntiles)
+                issue_tile<K, NT>(g, it, tbuf + b * 4 * TILE, &bars[b]);
+        }
+    }
+    __syncthreads();
+
+    Tile<K> t;
+    t.lane = threadIdx.x & 31;
+    t.warp = threadIdx.x >> 5;
+    t.nwarps = NT >> 5;
+    t.first = threadIdx.x == 0;
+    t.last = threadIdx.x == NT - 1;
+    t.lastj = -1;
+    t.validn = K;
+    const int cl = threadIdx.x * K;  // first cell of this thread within the tile
+    int buf = 0;
+    int i = 0;
+    for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x, ++i) {
+        const int b = i & 1;
+        double *sm = tbuf + b * 4 * TILE;
+        mbar_wait(&bars[b], (i >> 1) & 1);
+        const TileGeom tg = tile_geom(g, it, TILE);
+        const int64_t c0 = tg.L + cl;
+        if (threadIdx.x == 0)  // uniform skip decision (see chain_rk4_kernel)
+            s_skip = g.first_bad[tg.buf_id] != 0;
+        __syncthreads();
+        if (!s_skip) {
+            bool ok = true;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                t.C[j] = sm[TILE + cl + j];
+                t.md[j] = make_divisor(sm[cl + j]);
+                ok &= divisor_fast_ok(t.md[j]);
+            }
+            t.Cn = (cl + K < TILE) ? sm[TILE + cl + K] : 1.0;
+            double x[K], v[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                x[j] = sm[2 * TILE + cl + j];
+                v[j] = sm[3 * TILE + cl + j];
+            }
+            for (int64_t s = 0; s < g.nsteps; ++s)
+                step<K, false, false>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+            if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
+                // exact replay from the tile input still in shared memory
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    x[j] = sm[2 * TILE + cl + j];
+                    v[j] = sm[3 * TILE + cl + j];
+                }
+                for (int64_t s = 0; s < g.nsteps; ++s) {
+                    step<K, false, true>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+                    if (__syncthreads_or(owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
+                        if (threadIdx.x == 0)
+                            record_bad(&g.first_bad[tg.buf_id], g.step0 + s + 1);
+                        break;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const int64_t c = c0 + j;
+                if (c >= tg.own_start && c < tg.own_end) {
+                    g.xout[tg.base + c] = x[j];
+                    g.vout[tg.base + c] = v[j];
+                    if (g.xs) {
+                        g.xs[tg.base + c] = x[j];
+                        g.vs[tg.base + c] = v[j];
+                    }
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with buffer b
+        if (threadIdx.x == 0) {
+            const int64_t nx = it + 2 * int64_t(gridDim.x);
+            if (nx < ntiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_tile<K, NT>(g, nx, sm, &bars[b]);
+            }
+        }
+    }
+}
+
+constexpr int kPersistK = 8;
+template <int NT>
+constexpr size_t persist_smem() { return 2 * 4 * size_t(kPersistK) * NT * sizeof(double); }
+
+template <int NT>
+cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
+{
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto kern = chain_tiles_persistent<kPersistK, NT>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(persist_smem<NT>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, persist_smem<NT>());
+    const int64_t ntiles = g.tiles * g.nbuf;
+    const int64_t grid = std::min<int64_t>(ntiles, int64_t(sms) * std::max(per_sm, 1));
+    kern<<<static_cast<unsigned>(grid), NT, persist_smem<NT>(), stream>>>(g);
+    return cudaGetLastError();
+}
+
 template <int K>
 cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
 {
@@ -260,6 +461,17 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
 
 cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream)
 {
+    // Tiled runs of the default shape go through the persistent prefetching
+    // kernel when the bulk copies are 16-byte aligned (even offsets).
+    const int64_t TILE = int64_t(threads) * K;
+    const bool tiled = g.H > 0 || g.tiles > 1;
+    const bool aligned = (g.n % 2 == 0) && (g.own_lo % 2 == 0) && (g.W % 2 == 0) &&
+                         (g.H % 2 == 0) && g.n >= TILE;
+    static const bool disable = std::getenv("OSC_NO_PERSIST") != nullptr;
+    if (tiled && aligned && !disable && K == kPersistK && threads == 128)
+        return launch_persistent<128>(g, stream);
+    if (tiled && aligned && !disable && K == kPersistK && threads == 256)
+        return launch_persistent<256>(g, stream);
     switch (K) {
     case 1: return launch_k<1>(g, threads, stream);
     case 2: return launch_k<2>(g, threads, stream);

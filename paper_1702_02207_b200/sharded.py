@@ -84,7 +84,7 @@ class ShardedChain:
     # interior/edge split: an edge region is at least one tile of owned cells
     EDGE_CELLS = 4096  # >= any tile (K x threads) so interior tiles never slide into ghosts
 
-    def __init__(self, m, C, x0, v0, dt, *, halo_steps=16, group=None, device=None,
+    def __init__(self, m, C, x0, v0, dt, *, halo_steps=32, group=None, device=None,
                  advance=None, rank=None, world=None):
         self.group = group
         if rank is None:
@@ -246,7 +246,7 @@ class LocalShardGroup:
     this is safe to run with several shards on one device).
     """
 
-    def __init__(self, m, C, x0, v0, dt, shards: int, *, halo_steps=16, device=None,
+    def __init__(self, m, C, x0, v0, dt, shards: int, *, halo_steps=32, device=None,
                  advance=None):
         self.parts = [ShardedChain(m, C, x0, v0, dt, halo_steps=halo_steps, device=device,
                                    advance=advance, rank=r, world=shards)

@@ -29,6 +29,10 @@
  *     reference Trajectory's retention rule (oscillator.py:252, 261-262).
  *     Time labels are not produced on the device: the host accumulates
  *     t += dt exactly as the reference does (oscillator.py:231).
+ *   - Energies: es (may be NULL) receives energy() (oscillator.py:266-276)
+ *     of every retained sample, [1 + nsteps/stride][B], computed on the
+ *     device in the reference's sequential order (bit-identical) -- the
+ *     drift diagnostic without copying trajectories back.
  *   - All arithmetic is IEEE binary64 in the reference's operation order:
  *     results are byte-identical to oscbench.integrate.
  */
@@ -46,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 1
+#define OSC_ABI_VERSION 2
 
 int osc_abi_version(void);
 const char *osc_last_error(void);
@@ -57,7 +61,7 @@ const char *osc_last_error(void);
  * xs/vs: [1 + nsteps/stride][2][B].  first_bad: [B]. */
 int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                    double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                   int64_t *first_bad, void *stream);
+                   double *es, int64_t *first_bad, void *stream);
 
 /* B independent wall-anchored chains of s cells, layout [B][s]
  * (spring i joins cell i to cell i-1, spring 0 to the wall, last cell free;
@@ -68,7 +72,7 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
  * xs/vs: [1 + nsteps/stride][B][s].  first_bad: [B]. */
 int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B,
                    int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                   int64_t *first_bad, int64_t halo_steps, void *stream);
+                   double *es, int64_t *first_bad, int64_t halo_steps, void *stream);
 
 /* One temporally blocked launch over a chain shard buffer of n cells, used by
  * the multi-GPU driver: cells [own_lo, own_hi) are advanced nsteps steps from

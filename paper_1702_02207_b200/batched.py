@@ -70,6 +70,15 @@ class BatchResult:
     nsteps: int
     stride: int
     t0: float = 0.0
+    energies: torch.Tensor | None = None  # [nsamp][B] energy() of each sample
+
+    def energy_drift(self) -> torch.Tensor:
+        """max_k |E_k - E_0| / E_0 per system (harness.py:508-510's drift)."""
+        if self.energies is None:
+            raise ValueError("run with energies=True")
+        e0 = self.energies[0]
+        d = (self.energies - e0).abs().amax(dim=0)
+        return torch.where(e0 > 0, d / e0, d)
 
     def times(self) -> np.ndarray:
         return accumulated_times(self.t0, self.dt, self.nsteps, self.stride)
@@ -99,8 +108,14 @@ def _outputs(x0, v0, nsteps, stride, sample):
     return x, v, xs, vs
 
 
-def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, stream=None,
-                     check=True) -> BatchResult:
+def _energies(nsteps, stride, B, device, want):
+    if not want:
+        return None
+    return torch.empty((1 + nsteps // stride, B), dtype=torch.float64, device=device)
+
+
+def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
+                     stream=None, check=True) -> BatchResult:
     """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
@@ -109,17 +124,18 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, str
         raise ValueError(f"expected [2][B] arrays, got {tuple(m.shape)}")
     B = m.shape[1]
     x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
+    es = _energies(nsteps, stride, B, m.device, energies)
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
-    rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt),
-                                      int(nsteps), int(stride), _ptr(xs), _ptr(vs), _ptr(fb),
-                                      ctypes.c_void_p(_stream(stream)))
+    rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt), int(nsteps),
+                            int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb),
+                            ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_batch2")
-    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride))
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es)
     return res.check() if check else res
 
 
-def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, halo_steps=0,
-                     stream=None, check=True) -> BatchResult:
+def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
+                     halo_steps=0, stream=None, check=True) -> BatchResult:
     """B wall-anchored chains of s cells, ``[B][s]`` (oscillator.py:152-263)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
@@ -130,12 +146,13 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, hal
         raise ValueError(f"expected [B][s] arrays, got {tuple(m.shape)}")
     B, s = m.shape
     x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
+    es = _energies(nsteps, stride, B, m.device, energies)
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
-    rc = lib.osc_rk4_chains(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, s, float(dt),
-                                      int(nsteps), int(stride), _ptr(xs), _ptr(vs), _ptr(fb),
-                                      int(halo_steps), ctypes.c_void_p(_stream(stream)))
+    rc = lib.osc_rk4_chains(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, s, float(dt), int(nsteps),
+                            int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb),
+                            int(halo_steps), ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_chains")
-    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride))
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es)
     return res.check() if check else res
 
 

@@ -135,8 +135,8 @@ int osc_abi_version(void) { return OSC_ABI_VERSION; }
 const char *osc_last_error(void) { return g_last_error.c_str(); }
 
 int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B, double dt,
-                   int64_t nsteps, int64_t stride, double *xs, double *vs, int64_t *first_bad,
-                   void *stream)
+                   int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
+                   int64_t *first_bad, void *stream)
 {
     if (int rc = check_run_args(dt, nsteps, stride))
         return rc;
@@ -146,13 +146,13 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
         return OSC_OK;
     if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
-    cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs,
+    cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs, es,
                                        first_bad, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "batch2_rk4_kernel");
 }
 
 int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B, int64_t s,
-                   double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                   double dt, int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
                    int64_t *first_bad, int64_t halo_steps, void *stream_)
 {
     if (int rc = check_run_args(dt, nsteps, stride))
@@ -208,6 +208,11 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
         OSC_CUDA(cudaMemcpyAsync(xs, x, bytes, cudaMemcpyDeviceToDevice, stream));
         OSC_CUDA(cudaMemcpyAsync(vs, v, bytes, cudaMemcpyDeviceToDevice, stream));
     }
+    if (es) {  // energy() of every retained sample, exact sequential sum per chain
+        cudaError_t e = osc::launch_energy(m, C, x, v, es, B, s, false, stream);
+        if (e != cudaSuccess)
+            return cuda_fail(e, "energy_kernel");
+    }
     retain_pool_memory();
     Scratch scratch;
     scratch.s = stream;
@@ -232,6 +237,12 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
         cudaError_t e = osc::launch_chain(g, K, threads, stream);
         if (e != cudaSuccess)
             return cuda_fail(e, "chain_rk4_kernel");
+        if (es && (k0 + n) % stride == 0) {
+            e = osc::launch_energy(m, C, nx, nv, es + ((k0 + n) / stride) * B, B, s, false,
+                                   stream);
+            if (e != cudaSuccess)
+                return cuda_fail(e, "energy_kernel");
+        }
         std::swap(cx, nx);
         std::swap(cv, nv);
         k0 += n;
@@ -459,7 +470,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
             OSC_CUDA(cudaMemcpyAsync(dx + o, x + o, n, H2D, st));
             OSC_CUDA(cudaMemcpyAsync(dv + o, v + o, n, H2D, st));
             rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps, stride, dxs,
-                                dvs, dfb + b0, 0, st);
+                                dvs, nullptr, dfb + b0, 0, st);
             if (rc != OSC_OK)
                 return rc;
             OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));
@@ -473,7 +484,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
                 for (int r = 0; r < 2; ++r)
                     OSC_CUDA(cudaMemcpyAsync(ds[a] + o + r * nb, hs[a] + r * B + b0, n, H2D, st));
             rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride, dxs, dvs,
-                                dfb + b0, st);
+                                nullptr, dfb + b0, st);
             if (rc != OSC_OK)
                 return rc;
             for (int r = 0; r < 2; ++r) {

@@ -86,6 +86,20 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     s.v1 = add(s.v1, mul(k.dt6, sv1));
 }
 
+// energy() (oscillator.py:266-276) of one 2-DOF system, in the reference's
+// order: total += 0.5*m*v*v; total += 0.5*C*ext*ext, cell by cell.
+__device__ __forceinline__ double energy2(const Sys2 &s, double m0, double m1, double C0,
+                                          double C1)
+{
+    double total = 0.0;
+    total = add(total, mul(mul(mul(0.5, m0), s.v0), s.v0));
+    total = add(total, mul(mul(mul(0.5, C0), s.x0), s.x0));  // ext = x0 - 0.0 == x0
+    total = add(total, mul(mul(mul(0.5, m1), s.v1), s.v1));
+    const double e1 = sub(s.x1, s.x0);
+    total = add(total, mul(mul(mul(0.5, C1), e1), e1));
+    return total;
+}
+
 __device__ __forceinline__ bool finite2(const Sys2 &s)
 {
     return finite(s.x0) & finite(s.x1) & finite(s.v0) & finite(s.v1);
@@ -102,7 +116,8 @@ __global__ void __launch_bounds__(256)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
                   StepConsts k, int64_t nsteps, int64_t stride, double *__restrict__ xs,
-                  double *__restrict__ vs, int64_t *__restrict__ first_bad)
+                  double *__restrict__ vs, double *__restrict__ es,
+                  int64_t *__restrict__ first_bad)
 {
     const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * NS + threadIdx.x;
     int64_t idx[NS];
@@ -129,6 +144,8 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             vs[i] = s[j].v0;
             vs[B + i] = s[j].v1;
         }
+        if (es && live[j])
+            es[i] = energy2(s[j], m[i], m[B + i], C0[j], C1[j]);
     }
     int64_t bad[NS];
 #pragma unroll
@@ -179,16 +196,21 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             }
         }
         kstep += n;
-        if (xs && kstep % stride == 0) {
+        if ((xs || es) && kstep % stride == 0) {
             const int64_t o = (kstep / stride) * 2 * B;
 #pragma unroll
             for (int j = 0; j < NS; ++j) {
-                if (live[j]) {
+                if (live[j] && bad[j] == 0) {
                     const int64_t i = idx[j];
-                    xs[o + i] = s[j].x0;
-                    xs[o + B + i] = s[j].x1;
-                    vs[o + i] = s[j].v0;
-                    vs[o + B + i] = s[j].v1;
+                    if (xs) {
+                        xs[o + i] = s[j].x0;
+                        xs[o + B + i] = s[j].x1;
+                        vs[o + i] = s[j].v0;
+                        vs[o + B + i] = s[j].v1;
+                    }
+                    if (es)
+                        es[(kstep / stride) * B + i] =
+                            energy2(s[j], m0[j].b, m1[j].b, C0[j], C1[j]);
                 }
             }
         }
@@ -215,12 +237,12 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
 template <int NS>
 cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, int64_t B,
                       StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                      int64_t *first_bad, int threads, cudaStream_t stream)
+                      double *es, int64_t *first_bad, int threads, cudaStream_t stream)
 {
     const int64_t per_block = int64_t(threads) * NS;
     const int64_t blocks = (B + per_block - 1) / per_block;
     batch2_rk4_kernel<NS><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-        m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad);
+        m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
     return cudaGetLastError();
 }
 
@@ -228,7 +250,7 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
 
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                          int64_t *first_bad, cudaStream_t stream)
+                          double *es, int64_t *first_bad, cudaStream_t stream)
 {
     // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
     // overrides it for benchmarking (read-only process state).
@@ -249,9 +271,9 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
         }
     }
     switch (ns) {
-    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad, threads, stream);
-    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad, threads, stream);
-    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, first_bad, threads, stream);
+    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, stream);
+    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, stream);
+    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, stream);
     }
 }
 

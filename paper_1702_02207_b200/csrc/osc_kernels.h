@@ -25,7 +25,7 @@ struct SegArgs {
 
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                          int64_t *first_bad, cudaStream_t stream);
+                          double *es, int64_t *first_bad, cudaStream_t stream);
 
 cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream);
 

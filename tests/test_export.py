@@ -29,11 +29,12 @@ def test_csv_matches_reference_exporter(golden, tmp_path, name):
         pytest.skip("reference package not present")
     sys.path.insert(0, ref_src)
     import oscbench
+    from oscbench.harness import export_trajectory as ref_export
 
     theirs = tmp_path / "theirs.csv"
     rtraj = oscbench.Trajectory(tuple(oscbench.PhaseState(s.positions, s.velocities, s.time)
                                       for s in traj.samples), traj.dt, traj.stride)
-    oscbench.export_trajectory(rtraj, str(theirs))
+    ref_export(rtraj, str(theirs))
     assert ours.read_bytes() == theirs.read_bytes()
 
 

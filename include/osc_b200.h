@@ -99,6 +99,16 @@ int osc_rowscale(const double *K, const double *m, double *A, int64_t s, void *s
 int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, double dt,
                   int64_t nsteps, int64_t *first_bad, void *stream);
 
+/* The paper's thread-per-equation engine (run_parallel, parallel.py:395-573)
+ * on one warp: lane j % 32 owns first-order equation j, shared-memory double
+ * banks stand in for SharedPhase and __syncwarp for StageBarrier.  Bit-
+ * identical trajectory to integrate(); step_ns[nsteps] receives the
+ * %globaltimer duration of every step (the per-step latency the paper
+ * studies).  1 <= s <= 64.  xs/vs: [1 + nsteps/stride][s]; first_bad: [1]. */
+int osc_equation_engine(const double *m, const double *C, const double *x0, const double *v0,
+                        int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs,
+                        double *vs, int64_t *first_bad, int64_t *step_ns, void *stream);
+
 /* derivative() (oscillator.py:184-191): dvel[b][i] = acceleration_at(...).
  * cell_major != 0 selects the [s][B] layout (batched 2-DOF SoA). */
 int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,

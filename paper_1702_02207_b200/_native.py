@@ -32,6 +32,8 @@ SIGNATURES = {
                                              _dbl, _i64, _i64, _vp, _vp]),
     "osc_rowscale": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "osc_rk4_dense": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _dbl, _i64, _vp, _vp]),
+    "osc_equation_engine": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,
+                                           _vp, _vp, _vp, _vp]),
     "osc_derivative": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
     "osc_energy": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
     "osc_check_division": (ctypes.c_int, [_i64, ctypes.c_uint64, ctypes.c_int,

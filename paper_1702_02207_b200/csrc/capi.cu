@@ -341,6 +341,23 @@ int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, d
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "unpack_kernel");
 }
 
+int osc_equation_engine(const double *m, const double *C, const double *x0, const double *v0,
+                        int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs,
+                        double *vs, int64_t *first_bad, int64_t *step_ns, void *stream)
+{
+    if (int rc = check_run_args(dt, nsteps, stride))
+        return rc;
+    if (s < 1 || s > 64)
+        return fail(OSC_INVALID, "the one-warp equation engine takes 1 <= s <= 64, got %lld",
+                    (long long)s);
+    if (!m || !C || !x0 || !v0 || !first_bad || !step_ns || (!xs) != (!vs))
+        return fail(OSC_INVALID, "null buffer");
+    cudaError_t e = osc::launch_equation_engine(m, C, x0, v0, static_cast<int>(s), dt, nsteps,
+                                                stride, xs, vs, first_bad, step_ns,
+                                                static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "equation_engine_kernel");
+}
+
 int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,
                    int64_t s, int cell_major, void *stream)
 {

@@ -57,4 +57,9 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
 cudaError_t launch_dense_unpack(const double *BA, const double *Vp, double *X, double *V,
                                 int64_t s, int64_t N, int64_t Np, cudaStream_t stream);
 
+cudaError_t launch_equation_engine(const double *m, const double *C, const double *x0,
+                                   const double *v0, int s, double dt, int64_t nsteps,
+                                   int64_t stride, double *xs, double *vs, int64_t *first_bad,
+                                   int64_t *step_ns, cudaStream_t stream);
+
 }  // namespace osc

@@ -147,7 +147,7 @@ class Workload:
         elif name == "C3":
             arrays = workloads.c3()
             T = halo or 32
-            self.kernel = "chain_rk4_kernel<8>"
+            self.kernel = "chain_tiles_persistent<8,256>"
             self.launches = -(-p.nsteps // T)
             self.world = world
             self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",
@@ -515,6 +515,22 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(wl)
 
+    engine_line = None
+    if wl.name == "C1":
+        # The paper's architecture on the GPU: one warp, lanes as equations,
+        # __syncwarp as the stage barrier; per-step latency distribution.
+        from paper_1702_02207_b200 import engine
+        from paper_1702_02207_b200.oscillator import PhaseState, build_chain
+
+        m, C, x0, v0 = workloads.c1()
+        run = engine.run_equation_engine(build_chain(m, C), PhaseState(x0, v0), wl.dt, 100_000,
+                                         100_000, warmup=1000)
+        st = run.latency
+        engine_line = {"steps": 100_000, "warmup": 1000, "p50_ns": st.p50 * 1e9,
+                       "p90_ns": st.p90 * 1e9, "p99_ns": st.p99 * 1e9, "max_ns": st.max * 1e9,
+                       "mean_ns": st.mean * 1e9, "stddev_ns": st.stddev * 1e9,
+                       "timer": "%globaltimer around each step (lane 0)"}
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -584,6 +600,8 @@ def main():
         "clocks": clocks.summary(),
         "step_ms": step_ms,
     }
+    if engine_line:
+        line["equation_engine"] = engine_line
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

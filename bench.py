@@ -351,11 +351,13 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
         nb = min(B, max(cores * 256, 1024))
         cal_steps = min(wl.nsteps, 1000)
         t = time.perf_counter()
-        oracle.c_rk4_batch2_final(m[:, :nb], C[:, :nb], x0[:, :nb], v0[:, :nb], wl.dt, cal_steps)
+        oracle.c_rk4_batch2_final(m[:, :nb], C[:, :nb], x0[:, :nb], v0[:, :nb], wl.dt, cal_steps,
+                                  nthreads=cores)
         rate = 2 * nb * cal_steps / max(time.perf_counter() - t, 1e-6)
         nb = int(min(B, max(nb, budget_s * rate / (2 * wl.nsteps))))
         t = time.perf_counter()
-        oracle.c_rk4_batch2_final(m[:, :nb], C[:, :nb], x0[:, :nb], v0[:, :nb], wl.dt, wl.nsteps)
+        oracle.c_rk4_batch2_final(m[:, :nb], C[:, :nb], x0[:, :nb], v0[:, :nb], wl.dt, wl.nsteps,
+                                  nthreads=cores)
         el = time.perf_counter() - t
         done = 2 * nb * wl.nsteps
         sample = f"{nb} of {B} systems x {wl.nsteps} steps (full horizon)"
@@ -364,7 +366,8 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
         nb = max(cores, 8)
         steps = min(wl.nsteps, 1000)
         t = time.perf_counter()
-        oracle.c_rk4_chains(m[:nb], C[:nb], x0[:nb], v0[:nb], wl.dt, steps, sample=False)
+        oracle.c_rk4_chains(m[:nb], C[:nb], x0[:nb], v0[:nb], wl.dt, steps, sample=False,
+                            nthreads=cores)
         el = time.perf_counter() - t
         done = nb * s * steps
         sample = f"{nb} of {Bc} chains x {steps} of {wl.nsteps} steps"
@@ -374,6 +377,7 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
         m, K, X0, V0 = wl.host
         A = K / m[:, None]
         steps = 2
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
         t = time.perf_counter()
         oracle.dense_rk4(A, X0, V0, wl.dt, steps)
         el = time.perf_counter() - t
@@ -386,7 +390,7 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
         s = m.size
         steps = 20
         t = time.perf_counter()
-        oracle.c_rk4_chain_mt(m, C, x0, v0, wl.dt, steps)
+        oracle.c_rk4_chain_mt(m, C, x0, v0, wl.dt, steps, nthreads=cores)
         el = time.perf_counter() - t
         done = s * steps
         sample = f"full {s}-cell chain x {steps} of {wl.nsteps} steps"
@@ -395,6 +399,17 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
 
 
 # --------------------------------------------------------------------------
+
+def allreduce_max(value: float, device, backend: str) -> float:
+    """Max over ranks (device times are taken per rank; the job's is the max)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64,
+                     device=device if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
 
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -461,10 +476,19 @@ def main():
     import torch.distributed as dist
 
     world, rank, local = dist_setup()
+    # OSC_BENCH_BACKEND=gloo runs several ranks on fewer GPUs (rank -> GPU
+    # local % count) to exercise the multi-rank path on a one-GPU box; the
+    # kernels of different ranks never wait on one another.  Default: NCCL,
+    # one rank per GPU.
+    backend = os.environ.get("OSC_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     if world > 1 and args.config == "C1":
         raise SystemExit("C1 is one serial 2-DOF system: replicas only (DESIGN.md)")
 
@@ -494,18 +518,14 @@ def main():
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     dev_s = sum(step_ms) * 1e-3
     if world > 1:
-        t = torch.tensor([dev_s], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s = float(t.item())
+        dev_s = allreduce_max(dev_s, device, backend)
 
     e2e = None
     if not args.no_e2e:
         e2e_s, h2d, d2h = wl.e2e(max(1, min(args.steps, 5)), 1)
         n_e2e = max(1, min(args.steps, 5))
         if world > 1:
-            t = torch.tensor([e2e_s], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s = allreduce_max(e2e_s, device, backend)
         e2e = {"value": world * wl.dof_steps * n_e2e / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "timing": "wall clock around the synchronous host-pointer C-ABI call "
@@ -600,6 +620,9 @@ def main():
         "clocks": clocks.summary(),
         "step_ms": step_ms,
     }
+    if world > 1 and backend != "nccl":
+        line["note"] = f"{world} ranks over {backend} on {torch.cuda.device_count()} GPU(s): " \
+                       "a multi-rank path check, not a scaling measurement"
     if engine_line:
         line["equation_engine"] = engine_line
     print(json.dumps(line))

@@ -141,18 +141,28 @@ class ShardedChain:
     def _exchange(self, x, v):
         """Refresh both ghost zones of (x, v) from the neighbours' owned cells."""
         self.boundary(x, v)
-        ops = []
         left = self.rank - 1 if self.rank > 0 else None
         right = self.rank + 1 if self.rank < self.world - 1 else None
+        # NCCL moves device buffers directly; other backends (gloo) stage
+        # through host memory.
+        stage = self.cuda and dist.get_backend(self.group) != "nccl"
+        bufs = (self.send_l, self.recv_l, self.send_r, self.recv_r)
+        if stage:
+            bufs = tuple(b.cpu() for b in bufs)
+        send_l, recv_l, send_r, recv_r = bufs
+        ops = []
         if left is not None:
-            ops.append(dist.P2POp(dist.isend, self.send_l, left, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.recv_l, left, self.group))
+            ops.append(dist.P2POp(dist.isend, send_l, left, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv_l, left, self.group))
         if right is not None:
-            ops.append(dist.P2POp(dist.isend, self.send_r, right, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.recv_r, right, self.group))
+            ops.append(dist.P2POp(dist.isend, send_r, right, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv_r, right, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if stage:
+            self.recv_l.copy_(recv_l)
+            self.recv_r.copy_(recv_r)
         self.fill_ghosts(x, v, self.recv_l if left is not None else None,
                          self.recv_r if right is not None else None)
 

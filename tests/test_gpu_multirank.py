@@ -1,0 +1,80 @@
+"""Two real processes sharding one chain on the CUDA kernel (gloo transport,
+both ranks on cuda:0 -- the kernels of the two ranks never wait on each
+other; the host-driven exchange is the only coupling).  Byte-identical to
+the single-GPU integration."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+from conftest import bits  # noqa: E402
+
+
+def _chain(s, seed, stiff=None):
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(0.5, 2.0, s)
+    C = rng.uniform(500.0, 2000.0, s)
+    if stiff is not None:
+        C[stiff] = 1e8
+    return m, C, rng.standard_normal(s), rng.standard_normal(s)
+
+
+def _port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _worker(rank, world, port, s, nsteps, T, stiff, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1702_02207_b200 import sharded
+
+        sh = sharded.ShardedChain(*_chain(s, 21, stiff), 1e-3, halo_steps=T)
+        fb = sh.run(nsteps)
+        x, v = sh.gather()
+        if rank == 0:
+            q.put((fb, x.numpy(), v.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, s, nsteps, T, stiff=None):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.start_processes(_worker, args=(world, _port(), s, nsteps, T, stiff, q), nprocs=world,
+                       join=True, start_method="spawn")
+    return q.get()
+
+
+@pytest.mark.parametrize("world,T", [(2, 32), (3, 16)])
+def test_processes_share_a_chain_bit_identically(world, T):
+    from paper_1702_02207_b200 import batched
+
+    s, n = 200_000, 97
+    fb, x, v = _run(world, s, n, T)
+    ref = batched.integrate_chains(*_chain(s, 21), 1e-3, n)
+    assert fb == 0
+    assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
+
+
+def test_processes_report_first_divergence():
+    from paper_1702_02207_b200 import batched
+
+    s = 60_000
+    fb, _, _ = _run(2, s, 300, 32, stiff=50_000)
+    ref = batched.integrate_chains(*_chain(s, 21, 50_000), 1e-3, 300, check=False)
+    assert fb > 0 and fb == int(ref.first_bad[0])

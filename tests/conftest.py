@@ -34,3 +34,27 @@ def bits(a):
     import numpy as np
 
     return np.ascontiguousarray(np.asarray(a, dtype="<f8")).tobytes()
+
+
+def collect(worker, args, nprocs):
+    """Spawn nprocs ranks of worker(rank, *args, queue); return what rank 0
+    puts on the queue.  Reads before joining (results larger than a pipe
+    buffer would otherwise deadlock) and fails fast if a rank dies."""
+    import queue as queue_mod
+
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = mp.start_processes(worker, args=args + (q,), nprocs=nprocs, join=False,
+                               start_method="spawn")
+    while True:
+        try:
+            out = q.get(timeout=1.0)
+            break
+        except queue_mod.Empty:
+            if procs.join(timeout=0):  # raises if a rank failed
+                raise RuntimeError("ranks exited without a result")
+    while not procs.join():
+        pass
+    return out

@@ -9,16 +9,15 @@ import socket
 import numpy as np
 import pytest
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
 
 torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import torch.distributed as dist  # noqa: E402
-import torch.multiprocessing as mp  # noqa: E402
 
-from conftest import bits  # noqa: E402
+from conftest import bits, collect  # noqa: E402
 
 
 def _chain(s, seed, stiff=None):
@@ -53,11 +52,7 @@ def _worker(rank, world, port, s, nsteps, T, stiff, q):
 
 
 def _run(world, s, nsteps, T, stiff=None):
-    ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
-    mp.start_processes(_worker, args=(world, _port(), s, nsteps, T, stiff, q), nprocs=world,
-                       join=True, start_method="spawn")
-    return q.get()
+    return collect(_worker, (world, _port(), s, nsteps, T, stiff), world)
 
 
 @pytest.mark.parametrize("world,T", [(2, 32), (3, 16)])

@@ -13,11 +13,12 @@ import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
-import torch.multiprocessing as mp
 
 import oracle
-from conftest import bits
+from conftest import bits, collect
 from paper_1702_02207_b200 import sharded
+
+pytestmark = pytest.mark.timeout(300)
 
 
 def oracle_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
@@ -75,11 +76,7 @@ def _worker(rank, world, port, s, nsteps, T, edge, stiff, q):
 
 
 def _run_world(world, s, nsteps, T, edge=64, stiff=None):
-    ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
-    mp.start_processes(_worker, args=(world, _free_port(), s, nsteps, T, edge, stiff, q),
-                       nprocs=world, join=True, start_method="spawn")
-    return q.get()
+    return collect(_worker, (world, _free_port(), s, nsteps, T, edge, stiff), world)
 
 
 def test_layout():

@@ -21,7 +21,7 @@ namespace osc {
 namespace {
 
 // Default launch shape (profiles/r01 sweep).
-constexpr int kBatch2NS = 2, kBatch2Threads = 128;
+constexpr int kBatch2NS = 2, kBatch2Threads = 256;
 
 struct Sys2 {
     double x0, x1, v0, v1;

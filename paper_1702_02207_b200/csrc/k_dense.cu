@@ -82,25 +82,49 @@ struct DenseArgs {
     int64_t step;      // 1-based step index (divergence tag)
 };
 
-// Stage one BK-slab of A (rows m0..m0+BM) and of Bop (cols n0..n0+BN).
-__device__ __forceinline__ void load_stage(const DenseArgs &g, double *sA, double *sB,
-                                           int64_t m0, int64_t n0, int64_t k0)
-{
-    const int tid = threadIdx.x;
-    const int64_t ld2 = 2 * g.N;
+// Per-thread cp.async plan: the global source of each 16-byte chunk this
+// thread copies (advanced by one slab per issue) and its swizzled smem slot.
+struct LoadPlan {
+    static constexpr int NA = (BM * BK / 2) / THREADS, NB = (BK * BN / 2) / THREADS;
+    const double *a[NA];
+    const double *b[NB];
+    int sa[NA], sb[NB];
+    int64_t b_step;  // doubles between consecutive B slabs (BK rows of Bop)
+
+    __device__ __forceinline__ LoadPlan(const DenseArgs &g, int64_t m0, int64_t n0)
+    {
+        const int tid = threadIdx.x;
+        const int64_t ld2 = 2 * g.N;
 #pragma unroll
-    for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {  // A: BM rows x BK/2 chunks
-        const int c = tid + i * THREADS;
-        const int r = c / (BK / 2), q = c % (BK / 2);
-        cp_async16(sA + swz_a(r, 2 * q), g.A + (m0 + r) * g.s + k0 + 2 * q);
-    }
+        for (int i = 0; i < NA; ++i) {
+            const int c = tid + i * THREADS, r = c / (BK / 2), q = c % (BK / 2);
+            a[i] = g.A + (m0 + r) * g.s + 2 * q;
+            sa[i] = swz_a(r, 2 * q);
+        }
 #pragma unroll
-    for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {  // B: BK rows x BN/2 chunks
-        const int c = tid + i * THREADS;
-        const int r = c / (BN / 2), q = c % (BN / 2);
-        cp_async16(sB + swz_b(r, 2 * q), g.Bop + (k0 + r) * ld2 + n0 + 2 * q);
+        for (int i = 0; i < NB; ++i) {
+            const int c = tid + i * THREADS, r = c / (BN / 2), q = c % (BN / 2);
+            b[i] = g.Bop + r * ld2 + n0 + 2 * q;
+            sb[i] = swz_b(r, 2 * q);
+        }
+        b_step = BK * ld2;
     }
-}
+
+    // Issue the next slab into stage buffer st and advance the sources.
+    __device__ __forceinline__ void issue(double *stage)
+    {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            cp_async16(stage + sa[i], a[i]);
+            a[i] += BK;
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            cp_async16(stage + BM * BK + sb[i], b[i]);
+            b[i] += b_step;
+        }
+    }
+};
 
 template <int kStage>
 __global__ void __launch_bounds__(THREADS, 4) dense_rk4_gemm(DenseArgs g)
@@ -120,40 +144,51 @@ __global__ void __launch_bounds__(THREADS, 4) dense_rk4_gemm(DenseArgs g)
         for (int j = 0; j < 2; ++j)
             acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    LoadPlan plan(g, m0, n0);
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
         if (st < KT)
-            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * BK, m0, n0,
-                       st * BK);
+            plan.issue(smem + st * kStageDoubles);
         cp_commit();
     }
     const int ar = lane >> 2, ac = lane & 3;  // fragment coordinates
+    // Fragment offsets within a stage (loop-invariant, hoisted): A rows
+    // wm*32 + 8i + ar at k = 4q + ac; B row 4q + ac, cols wn*16 + 8j + ar.
+    const auto offa = [&](int q, int i) { return swz_a(wm * 32 + i * 8 + ar, 4 * q + ac); };
+    const auto offb = [&](int q, int j) {
+        return BM * BK + swz_b(4 * q + ac, wn * 16 + j * 8 + ar);
+    };
     for (int64_t kt = 0; kt < KT; ++kt) {
         cp_wait<STAGES - 2>();
         __syncthreads();
-        const int64_t nk = kt + STAGES - 1;
-        if (nk < KT) {
-            const int st = nk % STAGES;
-            load_stage(g, smem + st * kStageDoubles, smem + st * kStageDoubles + BM * BK, m0, n0,
-                       nk * BK);
-        }
+        if (kt + STAGES - 1 < KT)
+            plan.issue(smem + ((kt + STAGES - 1) % STAGES) * kStageDoubles);
         cp_commit();
-        const double *sA = smem + (kt % STAGES) * kStageDoubles;
-        const double *sB = sA + BM * BK;
+        const double *sb = smem + (kt % STAGES) * kStageDoubles;
+        // double-buffered fragments: load k-step kk+4 while kk's DMMAs issue
+        double af[2][4], bf[2][2];
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double af[4], bf[2];
+        for (int i = 0; i < 4; ++i)
+            af[0][i] = sb[offa(0, i)];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                af[i] = sA[swz_a(wm * 32 + i * 8 + ar, kk + ac)];
+        for (int j = 0; j < 2; ++j)
+            bf[0][j] = sb[offb(0, j)];
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-                bf[j] = sB[swz_b(kk + ac, wn * 16 + j * 8 + ar)];
+        for (int q = 0; q < BK / 4; ++q) {
+            const int cur = q & 1;
+            if (q + 1 < BK / 4) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    af[cur ^ 1][i] = sb[offa(q + 1, i)];
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    bf[cur ^ 1][j] = sb[offb(q + 1, j)];
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 2; ++j)
-                    dmma(acc[i][j], af[i], bf[j]);
+                    dmma(acc[i][j], af[cur][i], bf[cur][j]);
         }
     }
     cp_wait<0>();
@@ -175,6 +210,15 @@ __global__ void __launch_bounds__(THREADS, 4) dense_rk4_gemm(DenseArgs g)
     __syncthreads();
 
     const int64_t cb = n0 / BN;  // trajectory block
+    if constexpr (kStage == 2) {
+        // benchmark-only: plain GEMM store (no RK4 epilogue), to separate the
+        // main loop's efficiency from the fused epilogue's cost
+        for (int e = tid; e < BM * BN; e += THREADS) {
+            const int r = e / BN, c = e % BN;
+            g.BB[(m0 + r) * 2 * g.N + n0 + c] = sC[r * CS + c];
+        }
+        return;
+    }
     const double h = g.k.half_dt, dt = g.k.dt, dt6 = g.k.dt6;
     const int64_t ld2 = 2 * g.N;
     bool bad = false;
@@ -287,6 +331,15 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
     cudaFuncSetAttribute(dense_rk4_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
     const unsigned blocks = static_cast<unsigned>((sp / BM) * ((2 * Np) / BN));
+    if (std::getenv("OSC_DENSE_RAW")) {  // benchmark-only: GEMMs without the RK4 epilogue
+        cudaFuncSetAttribute(dense_rk4_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemBytes));
+        for (int64_t t = 0; t < 2 * nsteps; ++t) {
+            g.Bop = BA;
+            dense_rk4_gemm<2><<<blocks, THREADS, kSmemBytes, stream>>>(g);
+        }
+        return cudaGetLastError();
+    }
     for (int64_t t = 0; t < nsteps; ++t) {
         g.step = step0 + t + 1;
         g.Bop = BA;

@@ -1,0 +1,123 @@
+"""Edge cases of the GPU path against the byte-identical oracle: operands that
+leave the division fast path (zeros, subnormals, near-overflow, subnormal
+masses), sampling edge cases, odd chain lengths around the tile size, and
+divergence on the very first step.  Bar: byte-equal, same first bad step."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1702_02207_b200 import batched  # noqa: E402
+
+
+def _check_batch2(m, C, x0, v0, dt, nsteps, stride):
+    res = batched.integrate_batch2(m, C, x0, v0, dt, nsteps, stride, sample=True, check=False)
+    xs, vs, _, _, fb = oracle.c_rk4_batch2(m, C, x0, v0, dt, nsteps, stride)
+    got_fb = res.first_bad.cpu().numpy()
+    assert got_fb.tolist() == fb.tolist()
+    ok = fb == 0
+    gx, gv = res.xs.cpu().numpy(), res.vs.cpu().numpy()
+    assert bits(gx[..., ok]) == bits(xs[..., ok]) and bits(gv[..., ok]) == bits(vs[..., ok])
+    # samples strictly before each diverged system's bad step are exact too
+    for b in np.nonzero(~ok)[0]:
+        n_ok = 1 + (int(fb[b]) - 1) // stride
+        assert bits(gx[:n_ok, :, b]) == bits(xs[:n_ok, :, b])
+    return res, fb
+
+
+def test_slow_path_operands_batch2():
+    rng = np.random.default_rng(99)
+    B = 4096
+    m = rng.uniform(0.5, 2.0, (2, B))
+    C = rng.uniform(500.0, 2000.0, (2, B))
+    x0 = rng.standard_normal((2, B))
+    v0 = rng.standard_normal((2, B))
+    x0[:, 0:64] = 0.0                 # equilibrium: zero numerators every step
+    v0[:, 0:64] = 0.0
+    x0[0, 64:128] = -0.0              # signed zeros
+    x0[:, 128:192] = 1e-310           # subnormal positions: tiny numerators
+    v0[:, 128:192] = 0.0
+    x0[:, 192:256] = 1e-200           # tiny but normal
+    x0[:, 256:320] = 1e150            # huge but finite
+    m[:, 320:384] = 5e-324            # subnormal masses (valid: positive, finite)
+    m[:, 384:448] = 1e300             # huge masses
+    C[:, 448:512] = 1e-300            # tiny springs
+    _check_batch2(m, C, x0, v0, 1e-4, 500, 100)
+
+
+def test_stride_not_dividing_nsteps():
+    rng = np.random.default_rng(5)
+    m, C = rng.uniform(0.5, 2, (2, 1000)), rng.uniform(500, 2000, (2, 1000))
+    x0, v0 = rng.standard_normal((2, 1000)), np.zeros((2, 1000))
+    res, _ = _check_batch2(m, C, x0, v0, 1e-4, 1001, 300)
+    assert res.xs.shape[0] == 4
+    _, _, xf, vf, _ = oracle.c_rk4_batch2(m, C, x0, v0, 1e-4, 1001, sample=False)
+    assert bits(res.x.cpu().numpy()) == bits(xf)  # final state is step 1001, not a sample
+
+
+def test_divergence_on_first_step_and_overflow():
+    m = np.array([[1.0, 1.0, 1.0], [1.0, 1.0, 1.0]])
+    C = np.array([[1.0, 1e308, 1.0], [1.0, 1e308, 1.0]])
+    x0 = np.array([[1.0, 1.0, 1e308], [0.0, -1.0, -1e308]])
+    v0 = np.zeros((2, 3))
+    _, fb = _check_batch2(m, C, x0, v0, 1.0, 50, 1)
+    assert fb[1] == 1 and fb[2] >= 1
+
+
+@pytest.mark.parametrize("s", [2047, 2048, 2049, 2050, 4095, 4097, 6001])
+def test_chain_lengths_around_tile(s):
+    """Whole-chain vs tiled, persistent (even) vs plain tiled (odd) lengths."""
+    rng = np.random.default_rng(s)
+    m = rng.uniform(0.5, 2.0, s)
+    C = rng.uniform(500.0, 2000.0, s)
+    x0 = rng.standard_normal(s)
+    v0 = rng.standard_normal(s)
+    res = batched.integrate_chains(m, C, x0, v0, 1e-3, 130, 65, sample=True)
+    xs, vs, _, _, fb = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 130, 65)
+    assert bits(res.xs.cpu().numpy()) == bits(xs) and bits(res.vs.cpu().numpy()) == bits(vs)
+
+
+def test_chain_slow_path_cells():
+    """Zero / subnormal / signed-zero cells inside a long tiled chain force the
+    exact replay of their tiles; the bytes must not change."""
+    s = 9000
+    rng = np.random.default_rng(17)
+    m = rng.uniform(0.5, 2.0, s)
+    C = rng.uniform(500.0, 2000.0, s)
+    x0 = rng.standard_normal(s)
+    v0 = rng.standard_normal(s)
+    x0[1000:1500] = 0.0
+    v0[1000:1500] = 0.0
+    x0[3000:3010] = 1e-310
+    x0[5000] = -0.0
+    m[7000] = 5e-324
+    res = batched.integrate_chains(m, C, x0, v0, 1e-4, 200, check=False)
+    _, _, xo, vo, fb = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-4, 200,
+                                           sample=False)
+    assert int(res.first_bad[0]) == int(fb[0])
+    if fb[0] == 0:
+        assert bits(res.x.cpu().numpy()) == bits(xo) and bits(res.v.cpu().numpy()) == bits(vo)
+
+
+def test_many_small_chains_whole_chain_mode():
+    """B chains of odd small lengths (padded CTAs)."""
+    for s in (3, 17, 100, 513):
+        rng = np.random.default_rng(s)
+        B = 37
+        m = rng.uniform(0.5, 2.0, (B, s))
+        C = rng.uniform(500.0, 2000.0, (B, s))
+        x0 = rng.standard_normal((B, s))
+        v0 = rng.standard_normal((B, s))
+        x0[5] = 0.0
+        v0[5] = 0.0
+        res = batched.integrate_chains(m, C, x0, v0, 1e-3, 600)
+        _, _, xo, vo, _ = oracle.c_rk4_chains(m, C, x0, v0, 1e-3, 600, sample=False)
+        assert bits(res.x.cpu().numpy()) == bits(xo) and bits(res.v.cpu().numpy()) == bits(vo)

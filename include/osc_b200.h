@@ -50,7 +50,13 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 2
+#define OSC_ABI_VERSION 3
+
+/* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
+ * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
+ * to the reference (measured tolerance in DESIGN.md / tests/test_gpu_fma.py).
+ * 0 = the default, byte-identical arithmetic. */
+#define OSC_FMA 1u
 
 int osc_abi_version(void);
 const char *osc_last_error(void);
@@ -61,7 +67,7 @@ const char *osc_last_error(void);
  * xs/vs: [1 + nsteps/stride][2][B].  first_bad: [B]. */
 int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                    double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                   double *es, int64_t *first_bad, void *stream);
+                   double *es, int64_t *first_bad, uint32_t flags, void *stream);
 
 /* B independent wall-anchored chains of s cells, layout [B][s]
  * (spring i joins cell i to cell i-1, spring 0 to the wall, last cell free;
@@ -72,7 +78,8 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
  * xs/vs: [1 + nsteps/stride][B][s].  first_bad: [B]. */
 int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B,
                    int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                   double *es, int64_t *first_bad, int64_t halo_steps, void *stream);
+                   double *es, int64_t *first_bad, int64_t halo_steps, uint32_t flags,
+                   void *stream);
 
 /* One temporally blocked launch over a chain shard buffer of n cells, used by
  * the multi-GPU driver: cells [own_lo, own_hi) are advanced nsteps steps from
@@ -84,7 +91,7 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
 int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           const double *vin, double *xout, double *vout, int64_t n,
                           int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
-                          int64_t step0, int64_t *first_bad, void *stream);
+                          int64_t step0, int64_t *first_bad, uint32_t flags, void *stream);
 
 /* Dense general system M x'' + K x = 0 (BASELINE configs[4]; outside the
  * reference).  osc_rowscale: A = K / m[:, None] (IEEE division

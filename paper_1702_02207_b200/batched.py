@@ -115,7 +115,7 @@ def _energies(nsteps, stride, B, device, want):
 
 
 def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
-                     stream=None, check=True) -> BatchResult:
+                     fma=False, stream=None, check=True) -> BatchResult:
     """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
@@ -128,14 +128,14 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
     rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt), int(nsteps),
                             int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb),
-                            ctypes.c_void_p(_stream(stream)))
+                            _native.OSC_FMA if fma else 0, ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_batch2")
     res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es)
     return res.check() if check else res
 
 
 def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
-                     halo_steps=0, stream=None, check=True) -> BatchResult:
+                     halo_steps=0, fma=False, stream=None, check=True) -> BatchResult:
     """B wall-anchored chains of s cells, ``[B][s]`` (oscillator.py:152-263)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
@@ -150,19 +150,20 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
     rc = lib.osc_rk4_chains(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, s, float(dt), int(nsteps),
                             int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb),
-                            int(halo_steps), ctypes.c_void_p(_stream(stream)))
+                            int(halo_steps), _native.OSC_FMA if fma else 0,
+                            ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_chains")
     res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es)
     return res.check() if check else res
 
 
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None):
+                  stream=None, fma=False):
     """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance)."""
     rc = _native.lib().osc_rk4_chain_advance(
         _ptr(m), _ptr(C), _ptr(xin), _ptr(vin), _ptr(xout), _ptr(vout), m.numel(), int(own_lo),
         int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad),
-        ctypes.c_void_p(_stream(stream)))
+        _native.OSC_FMA if fma else 0, ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_chain_advance")
 
 

@@ -136,8 +136,10 @@ const char *osc_last_error(void) { return g_last_error.c_str(); }
 
 int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B, double dt,
                    int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
-                   int64_t *first_bad, void *stream)
+                   int64_t *first_bad, uint32_t flags, void *stream)
 {
+    if (flags & ~uint32_t(OSC_FMA))
+        return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, stride))
         return rc;
     if (B < 0)
@@ -147,14 +149,17 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
     if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs, es,
-                                       first_bad, static_cast<cudaStream_t>(stream));
+                                       first_bad, (flags & OSC_FMA) != 0,
+                                       static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "batch2_rk4_kernel");
 }
 
 int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B, int64_t s,
                    double dt, int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
-                   int64_t *first_bad, int64_t halo_steps, void *stream_)
+                   int64_t *first_bad, int64_t halo_steps, uint32_t flags, void *stream_)
 {
+    if (flags & ~uint32_t(OSC_FMA))
+        return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, stride))
         return rc;
     if (B < 0 || s < 1)
@@ -177,6 +182,7 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     g.own_lo = 0;
     g.own_hi = s;
     g.k = consts(dt);
+    g.fma = (flags & OSC_FMA) != 0;
     int K = kTileK, threads = kTileThreads;
     int64_t per_launch;
     int wk = 0, wt = 0;
@@ -257,8 +263,10 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
 int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, const double *vin,
                           double *xout, double *vout, int64_t n, int64_t own_lo, int64_t own_hi,
                           double dt, int64_t nsteps, int64_t step0, int64_t *first_bad,
-                          void *stream)
+                          uint32_t flags, void *stream)
 {
+    if (flags & ~uint32_t(OSC_FMA))
+        return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, 1))
         return rc;
     if (n < 1 || own_lo < 0 || own_hi > n || own_lo >= own_hi)
@@ -287,6 +295,7 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
     g.k = consts(dt);
     g.nsteps = nsteps;
     g.step0 = step0;
+    g.fma = (flags & OSC_FMA) != 0;
     cudaError_t e = osc::launch_chain(g, kTileK, kTileThreads, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "chain_rk4_kernel");
 }
@@ -487,7 +496,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
             OSC_CUDA(cudaMemcpyAsync(dx + o, x + o, n, H2D, st));
             OSC_CUDA(cudaMemcpyAsync(dv + o, v + o, n, H2D, st));
             rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps, stride, dxs,
-                                dvs, nullptr, dfb + b0, 0, st);
+                                dvs, nullptr, dfb + b0, 0, 0, st);
             if (rc != OSC_OK)
                 return rc;
             OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));
@@ -501,7 +510,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
                 for (int r = 0; r < 2; ++r)
                     OSC_CUDA(cudaMemcpyAsync(ds[a] + o + r * nb, hs[a] + r * B + b0, n, H2D, st));
             rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride, dxs, dvs,
-                                nullptr, dfb + b0, st);
+                                nullptr, dfb + b0, 0, st);
             if (rc != OSC_OK)
                 return rc;
             for (int r = 0; r < 2; ++r) {

@@ -27,63 +27,63 @@ struct Sys2 {
     double x0, x1, v0, v1;
 };
 
-template <bool kExact>
+template <Arith A>
 __device__ __forceinline__ void accel2(double p0, double p1, double C0, double C1,
                                        const Divisor &m0, const Divisor &m1, double &a0,
                                        double &a1, bool &ok)
 {
     const double d1 = sub(p1, p0);
     const double f1 = mul(C1, d1);
-    const double g0 = mul(-C0, p0);
-    a0 = qdiv<kExact>(add(g0, f1), m0, ok);
-    a1 = qdiv<kExact>(-f1, m1, ok);
+    const double num0 = (A == Arith::Fma) ? __fma_rn(-C0, p0, f1) : add(mul(-C0, p0), f1);
+    a0 = qdiv<A>(num0, m0, ok);
+    a1 = qdiv<A>(-f1, m1, ok);
 }
 
 // One classical RK4 step (oscillator.py:208-231).  The combination sums are
 // accumulated left to right exactly as combine_value's
 // ((k1 + 2k2) + 2k3) + k4; 2.0*k is exact.
-template <bool kExact>
+template <Arith A>
 __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divisor &m0,
                                       const Divisor &m1, const StepConsts &k, bool &ok)
 {
     double a0, a1;
     // k1 at the step start; position slopes are the velocities.
-    accel2<kExact>(s.x0, s.x1, C0, C1, m0, m1, a0, a1, ok);
+    accel2<A>(s.x0, s.x1, C0, C1, m0, m1, a0, a1, ok);
     double sx0 = s.v0, sx1 = s.v1, sv0 = a0, sv1 = a1;
-    double yv0 = add(s.v0, mul(k.half_dt, a0));
-    double yv1 = add(s.v1, mul(k.half_dt, a1));
-    double yp0 = add(s.x0, mul(k.half_dt, s.v0));
-    double yp1 = add(s.x1, mul(k.half_dt, s.v1));
+    double yv0 = stage<A>(s.v0, k.half_dt, a0);
+    double yv1 = stage<A>(s.v1, k.half_dt, a1);
+    double yp0 = stage<A>(s.x0, k.half_dt, s.v0);
+    double yp1 = stage<A>(s.x1, k.half_dt, s.v1);
     // k2 at the midpoint; y2v doubles as the k2 position slope.
-    accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
-    sx0 = add_twice_checked<kExact>(sx0, yv0, ok);
-    sx1 = add_twice_checked<kExact>(sx1, yv1, ok);
-    sv0 = add_twice<kExact>(sv0, a0);
-    sv1 = add_twice<kExact>(sv1, a1);
-    yp0 = add(s.x0, mul(k.half_dt, yv0));
-    yp1 = add(s.x1, mul(k.half_dt, yv1));
-    yv0 = add(s.v0, mul(k.half_dt, a0));
-    yv1 = add(s.v1, mul(k.half_dt, a1));
+    accel2<A>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
+    sx0 = add_twice_checked<A>(sx0, yv0, ok);
+    sx1 = add_twice_checked<A>(sx1, yv1, ok);
+    sv0 = add_twice<A>(sv0, a0);
+    sv1 = add_twice<A>(sv1, a1);
+    yp0 = stage<A>(s.x0, k.half_dt, yv0);
+    yp1 = stage<A>(s.x1, k.half_dt, yv1);
+    yv0 = stage<A>(s.v0, k.half_dt, a0);
+    yv1 = stage<A>(s.v1, k.half_dt, a1);
     // k3 at the refined midpoint.
-    accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
-    sx0 = add_twice_checked<kExact>(sx0, yv0, ok);
-    sx1 = add_twice_checked<kExact>(sx1, yv1, ok);
-    sv0 = add_twice<kExact>(sv0, a0);
-    sv1 = add_twice<kExact>(sv1, a1);
-    yp0 = add(s.x0, mul(k.dt, yv0));
-    yp1 = add(s.x1, mul(k.dt, yv1));
-    yv0 = add(s.v0, mul(k.dt, a0));
-    yv1 = add(s.v1, mul(k.dt, a1));
+    accel2<A>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
+    sx0 = add_twice_checked<A>(sx0, yv0, ok);
+    sx1 = add_twice_checked<A>(sx1, yv1, ok);
+    sv0 = add_twice<A>(sv0, a0);
+    sv1 = add_twice<A>(sv1, a1);
+    yp0 = stage<A>(s.x0, k.dt, yv0);
+    yp1 = stage<A>(s.x1, k.dt, yv1);
+    yv0 = stage<A>(s.v0, k.dt, a0);
+    yv1 = stage<A>(s.v1, k.dt, a1);
     // k4 at the endpoint, then the weighted combination.
-    accel2<kExact>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
+    accel2<A>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
     sx0 = add(sx0, yv0);
     sx1 = add(sx1, yv1);
     sv0 = add(sv0, a0);
     sv1 = add(sv1, a1);
-    s.x0 = add(s.x0, mul(k.dt6, sx0));
-    s.x1 = add(s.x1, mul(k.dt6, sx1));
-    s.v0 = add(s.v0, mul(k.dt6, sv0));
-    s.v1 = add(s.v1, mul(k.dt6, sv1));
+    s.x0 = stage<A>(s.x0, k.dt6, sx0);
+    s.x1 = stage<A>(s.x1, k.dt6, sx1);
+    s.v0 = stage<A>(s.v0, k.dt6, sv0);
+    s.v1 = stage<A>(s.v1, k.dt6, sv1);
 }
 
 // energy() (oscillator.py:266-276) of one 2-DOF system, in the reference's
@@ -111,7 +111,7 @@ constexpr int kChunk = 64;  // steps between divergence checks
 // system j of thread t in block b is b*NS*blockDim + j*blockDim + t, so each
 // load/store of a warp stays one contiguous 256 B run.  Indices past B
 // duplicate the last system and are never stored.
-template <int NS>
+template <int NS, bool kFma>
 __global__ void __launch_bounds__(256)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
@@ -169,7 +169,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             for (int t = 0; t < n; ++t) {
 #pragma unroll
                 for (int j = 0; j < NS; ++j)
-                    step2<false>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
+                    step2<kFma ? Arith::Fma : Arith::Fast>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
             }
 #pragma unroll
             for (int j = 0; j < NS; ++j)
@@ -187,7 +187,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             for (int t = 0; t < n; ++t) {
 #pragma unroll
                 for (int j = 0; j < NS; ++j) {
-                    step2<true>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
+                    step2<kFma ? Arith::Fma : Arith::Exact>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
                     if (bad[j] == 0 && !finite2(s[j])) {
                         bad[j] = kstep + t + 1;
                         exact_only = true;
@@ -237,12 +237,17 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
 template <int NS>
 cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, int64_t B,
                       StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                      double *es, int64_t *first_bad, int threads, cudaStream_t stream)
+                      double *es, int64_t *first_bad, int threads, bool fma,
+                      cudaStream_t stream)
 {
     const int64_t per_block = int64_t(threads) * NS;
-    const int64_t blocks = (B + per_block - 1) / per_block;
-    batch2_rk4_kernel<NS><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-        m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
+    const unsigned blocks = static_cast<unsigned>((B + per_block - 1) / per_block);
+    if (fma)
+        batch2_rk4_kernel<NS, true><<<blocks, threads, 0, stream>>>(
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
+    else
+        batch2_rk4_kernel<NS, false><<<blocks, threads, 0, stream>>>(
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
     return cudaGetLastError();
 }
 
@@ -250,7 +255,7 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
 
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                          double *es, int64_t *first_bad, cudaStream_t stream)
+                          double *es, int64_t *first_bad, bool fma, cudaStream_t stream)
 {
     // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
     // overrides it for benchmarking (read-only process state).
@@ -271,9 +276,9 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
         }
     }
     switch (ns) {
-    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, stream);
-    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, stream);
-    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, stream);
+    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream);
+    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream);
+    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream);
     }
 }
 

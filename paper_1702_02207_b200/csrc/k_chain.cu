@@ -51,7 +51,7 @@ struct Tile {
 // tile extends past the buffer end, so cells >= validn are padding whose
 // numerators are replaced by 1.0 (they never feed a real cell: the last real
 // cell has no right neighbour) to keep them off the slow division path.
-template <int K, bool kPad, bool kExact>
+template <int K, bool kPad, Arith A>
 __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], double (&a)[K],
                                       double (*s_lo)[kMaxWarps], double (*s_hi)[kMaxWarps],
                                       int &buf, bool &ok)
@@ -88,48 +88,48 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
         } else {
             num = t.last ? -f[j] : sub(fr, f[j]);
         }
-        a[j] = qdiv<kExact>(num, t.md[j], ok);
+        a[j] = qdiv<A>(num, t.md[j], ok);
     }
 }
 
 // One classical RK4 step (oscillator.py:208-231) of the thread's K cells.
-template <int K, bool kPad, bool kExact>
+template <int K, bool kPad, Arith A>
 __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&v)[K],
                                      const StepConsts &k, double (*s_lo)[kMaxWarps],
                                      double (*s_hi)[kMaxWarps], int &buf, bool &ok)
 {
     double a[K], yp[K], yv[K], sx[K], sv[K];
-    accel<K, kPad, kExact>(t, x, a, s_lo, s_hi, buf, ok);  // k1
+    accel<K, kPad, A>(t, x, a, s_lo, s_hi, buf, ok);  // k1
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = v[j];
         sv[j] = a[j];
-        yp[j] = add(x[j], mul(k.half_dt, v[j]));
-        yv[j] = add(v[j], mul(k.half_dt, a[j]));
+        yp[j] = stage<A>(x[j], k.half_dt, v[j]);
+        yv[j] = stage<A>(v[j], k.half_dt, a[j]);
     }
-    accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k2
+    accel<K, kPad, A>(t, yp, a, s_lo, s_hi, buf, ok);  // k2
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        sx[j] = add_twice_checked<kExact>(sx[j], yv[j], ok);
-        sv[j] = add_twice<kExact>(sv[j], a[j]);
-        yp[j] = add(x[j], mul(k.half_dt, yv[j]));
-        yv[j] = add(v[j], mul(k.half_dt, a[j]));
+        sx[j] = add_twice_checked<A>(sx[j], yv[j], ok);
+        sv[j] = add_twice<A>(sv[j], a[j]);
+        yp[j] = stage<A>(x[j], k.half_dt, yv[j]);
+        yv[j] = stage<A>(v[j], k.half_dt, a[j]);
     }
-    accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k3
+    accel<K, kPad, A>(t, yp, a, s_lo, s_hi, buf, ok);  // k3
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        sx[j] = add_twice_checked<kExact>(sx[j], yv[j], ok);
-        sv[j] = add_twice<kExact>(sv[j], a[j]);
-        yp[j] = add(x[j], mul(k.dt, yv[j]));
-        yv[j] = add(v[j], mul(k.dt, a[j]));
+        sx[j] = add_twice_checked<A>(sx[j], yv[j], ok);
+        sv[j] = add_twice<A>(sv[j], a[j]);
+        yp[j] = stage<A>(x[j], k.dt, yv[j]);
+        yv[j] = stage<A>(v[j], k.dt, a[j]);
     }
-    accel<K, kPad, kExact>(t, yp, a, s_lo, s_hi, buf, ok);  // k4
+    accel<K, kPad, A>(t, yp, a, s_lo, s_hi, buf, ok);  // k4
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], yv[j]);
         sv[j] = add(sv[j], a[j]);
-        x[j] = add(x[j], mul(k.dt6, sx[j]));
-        v[j] = add(v[j], mul(k.dt6, sv[j]));
+        x[j] = stage<A>(x[j], k.dt6, sx[j]);
+        v[j] = stage<A>(v[j], k.dt6, sv[j]);
     }
 }
 
@@ -161,9 +161,9 @@ __device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v
 
 // Register budget: K cells x ~10 live doubles per thread.
 template <int K>
-constexpr int max_threads() { return K <= 1 ? 1024 : K == 2 ? 512 : 256; }
+constexpr int max_threads() { return K <= 1 ? 1024 : K <= 4 ? 512 : 256; }
 
-template <int K, bool kPad>
+template <int K, bool kPad, bool kFma>
 __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 {
     __shared__ double s_lo[2][kMaxWarps];
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
     int buf = 0;
     bool ok = ok0;
     for (int64_t s = 0; s < g.nsteps; ++s)
-        step<K, kPad, false>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+        step<K, kPad, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, s_lo, s_hi, buf, ok);
 
     if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, own_start, own_end))) {
         // A division left nvcc's fast path, or a value went non-finite:
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
         // oscillator.py:255-260).
         load_state<K>(g, base, c0, cend, x, v);
         for (int64_t s = 0; s < g.nsteps; ++s) {
-            step<K, kPad, true>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+            step<K, kPad, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, s_lo, s_hi, buf, ok);
             if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
                 if (threadIdx.x == 0)
                     record_bad(&g.first_bad[buf_id], g.step0 + s + 1);
@@ -321,8 +321,8 @@ __device__ __forceinline__ void issue_tile(const SegArgs &g, int64_t it, double 
     bulk_g2s(dst + 3 * TILE, g.vin + o, bytes, bar);
 }
 
-template <int K, int NT>
-__global__ void __launch_bounds__(NT) chain_tiles_persistent(SegArgs g)
+template <int K, int NT, bool kFma>
+__global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_persistent(SegArgs g)
 {
     constexpr int64_t TILE = int64_t(NT) * K;
     extern __shared__ __align__(128) double tbuf[];  // 2 x [m | C | x | v] x TILE
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(NT) chain_tiles_persistent(SegArgs g)
                 v[j] = sm[3 * TILE + cl + j];
             }
             for (int64_t s = 0; s < g.nsteps; ++s)
-                step<K, false, false>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+                step<K, false, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, s_lo, s_hi, buf, ok);
             if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                 // exact replay from the tile input still in shared memory
 #pragma unroll
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(NT) chain_tiles_persistent(SegArgs g)
                     v[j] = sm[3 * TILE + cl + j];
                 }
                 for (int64_t s = 0; s < g.nsteps; ++s) {
-                    step<K, false, true>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+                    step<K, false, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, s_lo, s_hi, buf, ok);
                     if (__syncthreads_or(owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                         if (threadIdx.x == 0)
                             record_bad(&g.first_bad[tg.buf_id], g.step0 + s + 1);
@@ -421,23 +421,22 @@ __global__ void __launch_bounds__(NT) chain_tiles_persistent(SegArgs g)
     }
 }
 
-constexpr int kPersistK = 8;
-template <int NT>
-constexpr size_t persist_smem() { return 2 * 4 * size_t(kPersistK) * NT * sizeof(double); }
+template <int K, int NT>
+constexpr size_t persist_smem() { return 2 * 4 * size_t(K) * NT * sizeof(double); }
 
-template <int NT>
+template <int K, int NT>
 cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
 {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    auto kern = chain_tiles_persistent<kPersistK, NT>;
+    auto kern = g.fma ? chain_tiles_persistent<K, NT, true> : chain_tiles_persistent<K, NT, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(persist_smem<NT>()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, persist_smem<NT>());
+                         static_cast<int>(persist_smem<K, NT>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, persist_smem<K, NT>());
     const int64_t ntiles = g.tiles * g.nbuf;
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(sms) * std::max(per_sm, 1));
-    kern<<<static_cast<unsigned>(grid), NT, persist_smem<NT>(), stream>>>(g);
+    kern<<<static_cast<unsigned>(grid), NT, persist_smem<K, NT>(), stream>>>(g);
     return cudaGetLastError();
 }
 
@@ -451,9 +450,11 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
     const unsigned nb = static_cast<unsigned>(blocks);
     // Padding is needed only when a tile is longer than the whole buffer.
     if (TILE > g.n)
-        chain_rk4_kernel<K, true><<<nb, threads, 0, stream>>>(g);
+        (g.fma ? chain_rk4_kernel<K, true, true> : chain_rk4_kernel<K, true, false>)
+            <<<nb, threads, 0, stream>>>(g);
     else
-        chain_rk4_kernel<K, false><<<nb, threads, 0, stream>>>(g);
+        (g.fma ? chain_rk4_kernel<K, false, true> : chain_rk4_kernel<K, false, false>)
+            <<<nb, threads, 0, stream>>>(g);
     return cudaGetLastError();
 }
 
@@ -468,10 +469,16 @@ cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stre
     const bool aligned = (g.n % 2 == 0) && (g.own_lo % 2 == 0) && (g.W % 2 == 0) &&
                          (g.H % 2 == 0) && g.n >= TILE;
     static const bool disable = std::getenv("OSC_NO_PERSIST") != nullptr;
-    if (tiled && aligned && !disable && K == kPersistK && threads == 128)
-        return launch_persistent<128>(g, stream);
-    if (tiled && aligned && !disable && K == kPersistK && threads == 256)
-        return launch_persistent<256>(g, stream);
+    if (tiled && aligned && !disable) {
+        if (K == 8 && threads == 128)
+            return launch_persistent<8, 128>(g, stream);
+        if (K == 8 && threads == 256)
+            return launch_persistent<8, 256>(g, stream);
+        if (K == 4 && threads == 256)
+            return launch_persistent<4, 256>(g, stream);
+        if (K == 4 && threads == 512)
+            return launch_persistent<4, 512>(g, stream);
+    }
     switch (K) {
     case 1: return launch_k<1>(g, threads, stream);
     case 2: return launch_k<2>(g, threads, stream);

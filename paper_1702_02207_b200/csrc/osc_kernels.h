@@ -21,11 +21,12 @@ struct SegArgs {
     int64_t tiles;           // tiles per buffer
     StepConsts k;
     int64_t nsteps, step0;
+    bool fma;                // OSC_FMA mode (not bit-identical)
 };
 
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                          double *es, int64_t *first_bad, cudaStream_t stream);
+                          double *es, int64_t *first_bad, bool fma, cudaStream_t stream);
 
 cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream);
 

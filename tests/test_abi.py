@@ -48,18 +48,21 @@ def test_library_exports_every_declared_symbol(lib):
 def test_argument_errors_need_no_device(lib):
     # The reference's ValueError cases map to OSC_INVALID before any CUDA call.
     assert lib.osc_rk4_batch2(None, None, None, None, 4, float("nan"), 10, 1, None, None,
-                              None, None, None) == _native.OSC_INVALID
+                              None, None, 0, None) == _native.OSC_INVALID
     assert b"dt must be positive" in lib.osc_last_error()
     assert lib.osc_rk4_batch2(None, None, None, None, 4, 1e-3, 0, 1, None, None, None,
-                              None, None) == _native.OSC_INVALID
+                              None, 0, None) == _native.OSC_INVALID
     assert lib.osc_rk4_chains(None, None, None, None, 4, 3, 1e-3, 10, 0, None, None, None, None,
-                              0, None) == _native.OSC_INVALID
+                              0, 0, None) == _native.OSC_INVALID
     assert b"stride" in lib.osc_last_error()
     # empty batch is a no-op success, as an empty loop would be
     assert lib.osc_rk4_batch2(None, None, None, None, 0, 1e-3, 10, 1, None, None, None,
-                              None, None) == _native.OSC_OK
+                              None, 0, None) == _native.OSC_OK
+    assert lib.osc_rk4_batch2(None, None, None, None, 4, 1e-3, 10, 1, None, None, None,
+                              None, 0x80, None) == _native.OSC_INVALID
+    assert b"flags" in lib.osc_last_error()
     assert lib.osc_rk4_chain_advance(None, None, None, None, None, None, 100, 0, 100, 1e-3, 600,
-                                     0, None, None) == _native.OSC_INVALID
+                                     0, None, 0, None) == _native.OSC_INVALID
 
 
 def test_no_cpu_fallback():

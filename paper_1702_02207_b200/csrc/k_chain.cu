@@ -47,31 +47,38 @@ struct Tile {
     int lane, warp, nwarps;
 };
 
+// Warp-edge exchange slots, double-buffered by stage parity (compile-time:
+// a step has four stages, so parity restarts at 0 every step).  Slot w+1 of
+// [B][0] holds warp w's first position, of [B][1] its last; slots 0 and
+// nwarps+1 stay 0.0: the first cell then reads x_{-1} = 0.0 and
+// d_0 = x_0 - 0.0 == x_0 exactly (also for x_0 = -0.0), with no select.
+struct Edges {
+    double v[2][2][kMaxWarps + 2];
+};
+
 // acceleration_at for the K cells of this thread at positions p.  kPad: the
 // tile extends past the buffer end, so cells >= validn are padding whose
 // numerators are replaced by 1.0 (they never feed a real cell: the last real
 // cell has no right neighbour) to keep them off the slow division path.
-template <int K, bool kPad, Arith A>
+template <int K, bool kPad, Arith A, int B>
 __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], double (&a)[K],
-                                      double (*s_lo)[kMaxWarps], double (*s_hi)[kMaxWarps],
-                                      int &buf, bool &ok)
+                                      Edges &e, bool &ok)
 {
     double pl = __shfl_up_sync(kFull, p[K - 1], 1);
     double pr = __shfl_down_sync(kFull, p[0], 1);
     if (t.nwarps > 1) {
         if (t.lane == 0)
-            s_lo[buf][t.warp] = p[0];
+            e.v[B][0][t.warp + 1] = p[0];
         if (t.lane == 31)
-            s_hi[buf][t.warp] = p[K - 1];
+            e.v[B][1][t.warp + 1] = p[K - 1];
         __syncthreads();
-        if (t.lane == 0 && t.warp > 0)
-            pl = s_hi[buf][t.warp - 1];
-        if (t.lane == 31 && t.warp < t.nwarps - 1)
-            pr = s_lo[buf][t.warp + 1];
-        buf ^= 1;
+        if (t.lane == 31)
+            pr = e.v[B][0][t.warp + 2];
     }
+    if (t.lane == 0)
+        pl = e.v[B][1][t.warp];  // left neighbour's last position, or the 0.0 slot
     double f[K];
-    f[0] = mul(t.C[0], t.first ? p[0] : sub(p[0], pl));  // d_0 = x_0 - 0.0 == x_0
+    f[0] = mul(t.C[0], sub(p[0], pl));
 #pragma unroll
     for (int j = 1; j < K; ++j)
         f[j] = mul(t.C[j], sub(p[j], p[j - 1]));
@@ -92,14 +99,20 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
     }
 }
 
+// Zero every slot (sentinels included); callers then __syncthreads().
+__device__ __forceinline__ void edges_init(Edges &e)
+{
+    for (int i = threadIdx.x; i < 2 * 2 * (kMaxWarps + 2); i += blockDim.x)
+        (&e.v[0][0][0])[i] = 0.0;
+}
+
 // One classical RK4 step (oscillator.py:208-231) of the thread's K cells.
 template <int K, bool kPad, Arith A>
 __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&v)[K],
-                                     const StepConsts &k, double (*s_lo)[kMaxWarps],
-                                     double (*s_hi)[kMaxWarps], int &buf, bool &ok)
+                                     const StepConsts &k, Edges &e, bool &ok)
 {
     double a[K], yp[K], yv[K], sx[K], sv[K];
-    accel<K, kPad, A>(t, x, a, s_lo, s_hi, buf, ok);  // k1
+    accel<K, kPad, A, 0>(t, x, a, e, ok);  // k1
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = v[j];
@@ -107,7 +120,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
         yp[j] = stage<A>(x[j], k.half_dt, v[j]);
         yv[j] = stage<A>(v[j], k.half_dt, a[j]);
     }
-    accel<K, kPad, A>(t, yp, a, s_lo, s_hi, buf, ok);  // k2
+    accel<K, kPad, A, 1>(t, yp, a, e, ok);  // k2
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add_twice_checked<A>(sx[j], yv[j], ok);
@@ -115,7 +128,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
         yp[j] = stage<A>(x[j], k.half_dt, yv[j]);
         yv[j] = stage<A>(v[j], k.half_dt, a[j]);
     }
-    accel<K, kPad, A>(t, yp, a, s_lo, s_hi, buf, ok);  // k3
+    accel<K, kPad, A, 0>(t, yp, a, e, ok);  // k3
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add_twice_checked<A>(sx[j], yv[j], ok);
@@ -123,7 +136,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
         yp[j] = stage<A>(x[j], k.dt, yv[j]);
         yv[j] = stage<A>(v[j], k.dt, a[j]);
     }
-    accel<K, kPad, A>(t, yp, a, s_lo, s_hi, buf, ok);  // k4
+    accel<K, kPad, A, 1>(t, yp, a, e, ok);  // k4
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         sx[j] = add(sx[j], yv[j]);
@@ -166,14 +179,13 @@ constexpr int max_threads() { return K <= 1 ? 1024 : K <= 4 ? 512 : 256; }
 template <int K, bool kPad, bool kFma>
 __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 {
-    __shared__ double s_lo[2][kMaxWarps];
-    __shared__ double s_hi[2][kMaxWarps];
-
+    __shared__ Edges edges;
     __shared__ int s_skip;
     const int64_t buf_id = blockIdx.x / g.tiles;
     const int64_t tile = blockIdx.x % g.tiles;
     // One read, broadcast: another CTA may record a divergence at any time,
     // and the exit must be uniform across this CTA's barriers.
+    edges_init(edges);
     if (threadIdx.x == 0)
         s_skip = g.first_bad[buf_id] != 0;
     __syncthreads();
@@ -212,10 +224,9 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 
     double x[K], v[K];
     load_state<K>(g, base, c0, cend, x, v);
-    int buf = 0;
     bool ok = ok0;
     for (int64_t s = 0; s < g.nsteps; ++s)
-        step<K, kPad, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+        step<K, kPad, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, edges, ok);
 
     if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, own_start, own_end))) {
         // A division left nvcc's fast path, or a value went non-finite:
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
         // oscillator.py:255-260).
         load_state<K>(g, base, c0, cend, x, v);
         for (int64_t s = 0; s < g.nsteps; ++s) {
-            step<K, kPad, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+            step<K, kPad, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, edges, ok);
             if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
                 if (threadIdx.x == 0)
                     record_bad(&g.first_bad[buf_id], g.step0 + s + 1);
@@ -326,12 +337,12 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
 {
     constexpr int64_t TILE = int64_t(NT) * K;
     extern __shared__ __align__(128) double tbuf[];  // 2 x [m | C | x | v] x TILE
-    __shared__ double s_lo[2][kMaxWarps];
-    __shared__ double s_hi[2][kMaxWarps];
+    __shared__ Edges edges;
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ int s_skip;
 
     const int64_t ntiles = g.tiles * g.nbuf;
+    edges_init(edges);
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -353,7 +364,6 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
     t.lastj = -1;
     t.validn = K;
     const int cl = threadIdx.x * K;  // first cell of this thread within the tile
-    int buf = 0;
     int i = 0;
     for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x, ++i) {
         const int b = i & 1;
@@ -380,7 +390,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 v[j] = sm[3 * TILE + cl + j];
             }
             for (int64_t s = 0; s < g.nsteps; ++s)
-                step<K, false, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+                step<K, false, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, edges, ok);
             if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                 // exact replay from the tile input still in shared memory
 #pragma unroll
@@ -389,7 +399,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                     v[j] = sm[3 * TILE + cl + j];
                 }
                 for (int64_t s = 0; s < g.nsteps; ++s) {
-                    step<K, false, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, s_lo, s_hi, buf, ok);
+                    step<K, false, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, edges, ok);
                     if (__syncthreads_or(owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                         if (threadIdx.x == 0)
                             record_bad(&g.first_bad[tg.buf_id], g.step0 + s + 1);

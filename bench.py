@@ -660,6 +660,8 @@ def main():
     if fma_line:
         line["fma_mode"] = fma_line
     print(json.dumps(line))
+    if getattr(wl, "shard", None) is not None:
+        wl.shard.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 3
+#define OSC_ABI_VERSION 4
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -81,17 +81,31 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
                    double *es, int64_t *first_bad, int64_t halo_steps, uint32_t flags,
                    void *stream);
 
+/* A neighbouring shard's next-input buffers for the fused halo exchange:
+ * `count` boundary cells of ours (our first `count` owned cells for the left
+ * neighbour, our last `count` for the right one) are stored, by the same
+ * kernel that computes them, at x[c + offset] / v[c + offset], c being our
+ * buffer index -- peer memory over NVLink (CUDA IPC) or a local buffer. */
+typedef struct {
+    double *x, *v;
+    int64_t offset;
+    int64_t count;
+} osc_peer_t;
+
 /* One temporally blocked launch over a chain shard buffer of n cells, used by
  * the multi-GPU driver: cells [own_lo, own_hi) are advanced nsteps steps from
- * (xin, vin) into (xout, vout); the cells outside are ghosts copied from the
+ * (xin, vin) into (xout, vout); the cells outside are ghosts of the
  * neighbouring shards.  Buffer cell 0 is treated as wall-adjacent and cell
  * n-1 as the free end, which is exact at the true chain ends and, elsewhere,
  * harmless as long as each ghost zone is at least 2*nsteps cells wide.
+ * left/right (may be NULL): write our boundary cells straight into the
+ * neighbours' next-input ghost zones (no separate exchange).
  * first_bad: [1], updated to the minimum bad step (global step0 + j). */
 int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           const double *vin, double *xout, double *vout, int64_t n,
                           int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
-                          int64_t step0, int64_t *first_bad, uint32_t flags, void *stream);
+                          int64_t step0, int64_t *first_bad, const osc_peer_t *left,
+                          const osc_peer_t *right, uint32_t flags, void *stream);
 
 /* Dense general system M x'' + K x = 0 (BASELINE configs[4]; outside the
  * reference).  osc_rowscale: A = K / m[:, None] (IEEE division
@@ -115,6 +129,21 @@ int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, d
 int osc_equation_engine(const double *m, const double *C, const double *x0, const double *v0,
                         int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs,
                         double *vs, int64_t *first_bad, int64_t *step_ns, void *stream);
+
+/* Peer memory for the fused halo exchange between processes (one per GPU):
+ * plain device allocations whose CUDA IPC handles (64 bytes) are exchanged
+ * out of band, mapped by the neighbours (NVLink peer access), and
+ * interprocess events that order a neighbour's launch after ours. */
+int osc_device_alloc(uint64_t bytes, void **ptr);
+int osc_device_free(void *ptr);
+int osc_ipc_export(const void *ptr, unsigned char *handle64);
+int osc_ipc_import(const unsigned char *handle64, void **ptr);
+int osc_ipc_close(void *ptr);
+int osc_ipc_event_create(void **event, unsigned char *handle64);
+int osc_ipc_event_open(const unsigned char *handle64, void **event);
+int osc_event_record(void *event, void *stream);
+int osc_stream_wait_event(void *stream, void *event);
+int osc_event_destroy(void *event);
 
 /* derivative() (oscillator.py:184-191): dvel[b][i] = acceleration_at(...).
  * cell_major != 0 selects the [s][B] layout (batched 2-DOF SoA). */

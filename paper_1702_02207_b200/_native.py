@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
-ABI_VERSION = 3
+ABI_VERSION = 4
 OSC_FMA = 1
 
 _i64 = ctypes.c_int64
@@ -30,11 +30,22 @@ SIGNATURES = {
     "osc_rk4_chains": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64, _vp,
                                       _vp, _vp, _vp, _i64, ctypes.c_uint32, _vp]),
     "osc_rk4_chain_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
-                                             _dbl, _i64, _i64, _vp, ctypes.c_uint32, _vp]),
+                                             _dbl, _i64, _i64, _vp, _vp, _vp, ctypes.c_uint32,
+                                             _vp]),
     "osc_rowscale": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "osc_rk4_dense": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _dbl, _i64, _vp, _vp]),
     "osc_equation_engine": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,
                                            _vp, _vp, _vp, _vp]),
+    "osc_device_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    "osc_device_free": (ctypes.c_int, [_vp]),
+    "osc_ipc_export": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "osc_ipc_import": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "osc_ipc_close": (ctypes.c_int, [_vp]),
+    "osc_ipc_event_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p]),
+    "osc_ipc_event_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "osc_event_record": (ctypes.c_int, [_vp, _vp]),
+    "osc_stream_wait_event": (ctypes.c_int, [_vp, _vp]),
+    "osc_event_destroy": (ctypes.c_int, [_vp]),
     "osc_derivative": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
     "osc_energy": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
     "osc_check_division": (ctypes.c_int, [_i64, ctypes.c_uint64, ctypes.c_int,
@@ -46,6 +57,13 @@ SIGNATURES = {
     "osc_rk4_chains_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64,
                                            _vp, _vp, _vp]),
 }
+
+
+class Peer(ctypes.Structure):
+    """osc_peer_t: a neighbour's next-input buffers for the fused exchange."""
+
+    _fields_ = [("x", ctypes.c_void_p), ("v", ctypes.c_void_p), ("offset", ctypes.c_int64),
+                ("count", ctypes.c_int64)]
 
 
 class NativeUnavailableError(RuntimeError):

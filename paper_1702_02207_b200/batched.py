@@ -158,11 +158,18 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
 
 
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None, fma=False):
-    """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance)."""
+                  stream=None, fma=False, left=None, right=None):
+    """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance).
+
+    ``left``/``right``: optional ``(x, v, offset, count)`` -- a neighbour's
+    next-input buffers (data pointers) that receive our boundary cells from
+    the same kernel (the fused halo exchange)."""
+    peers = []
+    for p in (left, right):
+        peers.append(ctypes.byref(_native.Peer(*p)) if p is not None else None)
     rc = _native.lib().osc_rk4_chain_advance(
         _ptr(m), _ptr(C), _ptr(xin), _ptr(vin), _ptr(xout), _ptr(vout), m.numel(), int(own_lo),
-        int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad),
+        int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad), peers[0], peers[1],
         _native.OSC_FMA if fma else 0, ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_chain_advance")
 

@@ -263,7 +263,8 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
 int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, const double *vin,
                           double *xout, double *vout, int64_t n, int64_t own_lo, int64_t own_hi,
                           double dt, int64_t nsteps, int64_t step0, int64_t *first_bad,
-                          uint32_t flags, void *stream)
+                          const osc_peer_t *left, const osc_peer_t *right, uint32_t flags,
+                          void *stream)
 {
     if (flags & ~uint32_t(OSC_FMA))
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
@@ -296,6 +297,17 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
     g.nsteps = nsteps;
     g.step0 = step0;
     g.fma = (flags & OSC_FMA) != 0;
+    const osc_peer_t *peers[2] = {left, right};
+    for (int side = 0; side < 2; ++side) {
+        const osc_peer_t *p = peers[side];
+        if (!p || !p->x)
+            continue;
+        if (!p->v || p->count < 0 || p->count > own_hi - own_lo)
+            return fail(OSC_INVALID, "bad peer ghost descriptor");
+        // left neighbour receives our first `count` owned cells, right our last
+        const int64_t lo = side == 0 ? own_lo : own_hi - p->count;
+        g.peer[side] = osc::PeerGhost{p->x, p->v, p->offset, lo, lo + p->count};
+    }
     cudaError_t e = osc::launch_chain(g, kTileK, kTileThreads, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "chain_rk4_kernel");
 }
@@ -365,6 +377,86 @@ int osc_equation_engine(const double *m, const double *C, const double *x0, cons
                                                 stride, xs, vs, first_bad, step_ns,
                                                 static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "equation_engine_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Peer memory for the fused halo exchange: plain allocations (so an exported
+// pointer is an allocation base), CUDA IPC handles and interprocess events.
+// ---------------------------------------------------------------------------
+int osc_device_alloc(uint64_t bytes, void **ptr)
+{
+    if (!ptr)
+        return fail(OSC_INVALID, "null ptr");
+    OSC_CUDA(cudaMalloc(ptr, bytes));
+    return OSC_OK;
+}
+
+int osc_device_free(void *ptr)
+{
+    OSC_CUDA(cudaFree(ptr));
+    return OSC_OK;
+}
+
+int osc_ipc_export(const void *ptr, unsigned char *handle64)
+{
+    cudaIpcMemHandle_t h;
+    OSC_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)));
+    std::memcpy(handle64, &h, sizeof h);
+    return OSC_OK;
+}
+
+int osc_ipc_import(const unsigned char *handle64, void **ptr)
+{
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    OSC_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return OSC_OK;
+}
+
+int osc_ipc_close(void *ptr)
+{
+    OSC_CUDA(cudaIpcCloseMemHandle(ptr));
+    return OSC_OK;
+}
+
+int osc_ipc_event_create(void **event, unsigned char *handle64)
+{
+    cudaEvent_t ev;
+    OSC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));
+    cudaIpcEventHandle_t h;
+    OSC_CUDA(cudaIpcGetEventHandle(&h, ev));
+    std::memcpy(handle64, &h, sizeof h);
+    *event = ev;
+    return OSC_OK;
+}
+
+int osc_ipc_event_open(const unsigned char *handle64, void **event)
+{
+    cudaIpcEventHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    cudaEvent_t ev;
+    OSC_CUDA(cudaIpcOpenEventHandle(&ev, h));
+    *event = ev;
+    return OSC_OK;
+}
+
+int osc_event_record(void *event, void *stream)
+{
+    OSC_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)));
+    return OSC_OK;
+}
+
+int osc_stream_wait_event(void *stream, void *event)
+{
+    OSC_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream),
+                                 static_cast<cudaEvent_t>(event), 0));
+    return OSC_OK;
+}
+
+int osc_event_destroy(void *event)
+{
+    OSC_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+    return OSC_OK;
 }
 
 int osc_derivative(const double *m, const double *C, const double *x, double *dvel, int64_t B,

@@ -146,6 +146,28 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
     }
 }
 
+// Store an owned cell: own output, optional sample slot, and -- for cells in
+// a neighbour's ghost range -- straight into that neighbour's next-input
+// buffer (the fused compute + halo exchange over peer memory).
+__device__ __forceinline__ void store_owned(const SegArgs &g, int64_t base, int64_t c, double x,
+                                            double v)
+{
+    g.xout[base + c] = x;
+    g.vout[base + c] = v;
+    if (g.xs) {
+        g.xs[base + c] = x;
+        g.vs[base + c] = v;
+    }
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        const PeerGhost &p = g.peer[side];
+        if (p.x && c >= p.lo && c < p.hi) {
+            p.x[c + p.offset] = x;
+            p.v[c + p.offset] = v;
+        }
+    }
+}
+
 template <int K>
 __device__ __forceinline__ void load_state(const SegArgs &g, int64_t base, int64_t c0,
                                            int64_t cend, double (&x)[K], double (&v)[K])
@@ -247,14 +269,8 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int64_t c = c0 + j;
-        if (c >= own_start && c < own_end) {
-            g.xout[base + c] = x[j];
-            g.vout[base + c] = v[j];
-            if (g.xs) {
-                g.xs[base + c] = x[j];
-                g.vs[base + c] = v[j];
-            }
-        }
+        if (c >= own_start && c < own_end)
+            store_owned(g, base, c, x[j], v[j]);
     }
 }
 
@@ -410,14 +426,8 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
 #pragma unroll
             for (int j = 0; j < K; ++j) {
                 const int64_t c = c0 + j;
-                if (c >= tg.own_start && c < tg.own_end) {
-                    g.xout[tg.base + c] = x[j];
-                    g.vout[tg.base + c] = v[j];
-                    if (g.xs) {
-                        g.xs[tg.base + c] = x[j];
-                        g.vs[tg.base + c] = v[j];
-                    }
-                }
+                if (c >= tg.own_start && c < tg.own_end)
+                    store_owned(g, tg.base, c, x[j], v[j]);
             }
         }
         __syncthreads();  // every thread is done with buffer b

@@ -8,6 +8,14 @@
 
 namespace osc {
 
+// A neighbouring shard's next-input buffers (peer memory over NVLink, or a
+// local buffer): owned cells [lo, hi) of this shard are also stored at
+// x[c + offset], v[c + offset] -- the neighbour's ghost zone.
+struct PeerGhost {
+    double *x, *v;
+    int64_t offset, lo, hi;
+};
+
 // One launch of the chain kernel over nbuf buffers of n cells each.
 struct SegArgs {
     const double *m, *C;     // [nbuf][n]
@@ -22,6 +30,7 @@ struct SegArgs {
     StepConsts k;
     int64_t nsteps, step0;
     bool fma;                // OSC_FMA mode (not bit-identical)
+    PeerGhost peer[2];       // left / right neighbour ghost targets (x == nullptr: none)
 };
 
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,

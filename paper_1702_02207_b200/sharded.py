@@ -11,11 +11,22 @@ any number of ranks -- the GPU form of the reference engine's
 "bitwise-identical for every worker count" contract (parallel.py:11-14,
 test_parallel.py:259-271).
 
-Per period the exchange overlaps compute: the interior tiles (which read no
-ghost cell) are launched first, the ghost exchange runs on a side stream
-(NCCL send/recv of 2 x g doubles per neighbour), and the two edge tiles are
-launched after it.  The plumbing is ``torch.distributed`` (NCCL on GPUs, gloo
-in the CPU tests, where ``advance`` is injected).
+Two transports:
+
+* ``"nccl"`` (default): per period the interior tiles (which read no ghost
+  cell) are launched first, the ghost exchange runs on a side stream (NCCL
+  send/recv of 2 x g doubles per neighbour; gloo stages through the host),
+  and the two edge tiles are launched after it.
+* ``"peer"``: the fused compute + exchange.  Each rank maps its neighbours'
+  state buffers (CUDA IPC; NVLink peer memory between GPUs) and the tile
+  kernel itself stores its boundary cells into the neighbours' next-input
+  ghost zones (``osc_peer_t``), so there is no exchange step at all.  Order is
+  kept with device-side dependencies only: a rank's period-p launch waits
+  (``cudaStreamWaitEvent`` on interprocess events) for its neighbours'
+  period-(p-1) launches, which both produced its ghosts and finished reading
+  the buffer it is about to write into (ping-pong buffers).  A host barrier on
+  a gloo group orders event records before waits; the GPUs never wait on one
+  another inside a kernel.
 """
 
 from __future__ import annotations
@@ -66,11 +77,11 @@ def layout(s: int, rank: int, world: int, halo_steps: int) -> ShardLayout:
 
 
 def _cuda_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None):
+                  stream=None, left=None, right=None):
     from . import batched
 
     batched.chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
-                          first_bad, stream=stream)
+                          first_bad, stream=stream, left=left, right=right)
 
 
 class ShardedChain:
@@ -85,8 +96,12 @@ class ShardedChain:
     EDGE_CELLS = 4096  # >= any tile (K x threads) so interior tiles never slide into ghosts
 
     def __init__(self, m, C, x0, v0, dt, *, halo_steps=32, group=None, device=None,
-                 advance=None, rank=None, world=None):
+                 advance=None, rank=None, world=None, transport="nccl"):
+        if transport not in ("nccl", "peer"):
+            raise ValueError(f"transport must be 'nccl' or 'peer', got {transport!r}")
+        self.transport = transport
         self.group = group
+        distributed = rank is None  # rank/world given explicitly: an in-process shard
         if rank is None:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -116,6 +131,108 @@ class ShardedChain:
         self.recv_r = torch.empty_like(self.send_l)
         self.cuda = self.device.type == "cuda"
         self.comm_stream = torch.cuda.Stream(self.device) if self.cuda else None
+        self.peer_bufs = {}  # neighbour rank -> ((x, v) of its buffer 0, (x, v) of buffer 1, blo)
+        if transport == "peer" and self.world > 1 and dist.is_initialized() and distributed:
+            self._setup_peer()
+
+    # -- fused exchange over peer memory --------------------------------------
+    def peer_descriptors(self, p):
+        """(left, right) osc_peer_t tuples for period p: the neighbours' buffer
+        (p+1) % 2 -- the one they read next period -- and our cell offsets."""
+        g = self.L.g
+        out = []
+        for nb in (self.rank - 1, self.rank + 1):
+            if nb not in self.peer_bufs:
+                out.append(None)
+                continue
+            bufs, nblo = self.peer_bufs[nb]
+            x, v = bufs[(p + 1) % 2]
+            ptr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
+            out.append((ptr(x), ptr(v), self.L.blo - nblo, g))
+        return tuple(out)
+
+    def _setup_peer(self):
+        """Own state in exportable allocations; map the neighbours' state buffers
+        and events (CUDA IPC: NVLink peer memory between GPUs)."""
+        from . import peer
+
+        self.host_group = dist.new_group(backend="gloo")
+        n = self.L.n
+        self._own = [peer.DeviceVector(n, self.device) for _ in range(4)]
+        for dst, src in zip(self._own, (self.x, self.v, self.x2, self.v2)):
+            dst.tensor.copy_(src)
+        self.x, self.v, self.x2, self.v2 = (b.tensor for b in self._own)
+        self.events = [peer.IpcEvent() for _ in range(2)]
+        torch.cuda.synchronize(self.device)
+        mine = {"blo": self.L.blo, "bufs": [b.handle() for b in self._own],
+                "events": [e.handle for e in self.events]}
+        infos = [None] * self.world
+        dist.all_gather_object(infos, mine, group=self.host_group)
+        self.peer_events = {}
+        self._imported = []
+        for nb in (self.rank - 1, self.rank + 1):
+            if 0 <= nb < self.world:
+                ptrs = [peer.import_buffer(h) for h in infos[nb]["bufs"]]
+                self._imported += ptrs
+                self.peer_bufs[nb] = (((ptrs[0], ptrs[1]), (ptrs[2], ptrs[3])), infos[nb]["blo"])
+                self.peer_events[nb] = [peer.IpcEvent(h) for h in infos[nb]["events"]]
+
+    def close(self):
+        """Release peer resources in a safe order: finish local work, unmap the
+        neighbours' buffers and close their events, wait until every rank has
+        done so, then free the buffers and events this rank exported."""
+        if not getattr(self, "_own", None):
+            return
+        from . import peer
+
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.host_group)  # no rank still writes into anyone
+        for ptr in self._imported:
+            peer.close_buffer(ptr)
+        for evs in self.peer_events.values():
+            for ev in evs:
+                ev.destroy()
+        self._imported, self.peer_events = [], {}
+        self.peer_bufs.clear()
+        dist.barrier(group=self.host_group)  # every mapping of our memory is gone
+        # keep the results readable: move them to ordinary tensors first
+        self.x, self.v, self.x2, self.v2 = (t.clone() for t in (self.x, self.v, self.x2,
+                                                                 self.v2))
+        torch.cuda.synchronize(self.device)
+        for b in self._own:
+            b.free()
+        for ev in self.events:
+            ev.destroy()
+        self._own = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _run_peer(self, nsteps):
+        main = torch.cuda.current_stream(self.device)
+        a, b = self.L.own
+        k = p = 0
+        while k < nsteps:
+            n = min(self.T, nsteps - k)
+            if p > 0:  # neighbours' period p-1 wrote our ghosts and left their buffer
+                for evs in self.peer_events.values():
+                    evs[(p - 1) % 2].wait(main)
+            left, right = self.peer_descriptors(p)
+            self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, k,
+                         self.first_bad, left=left, right=right)
+            self.events[p % 2].record(main)
+            dist.barrier(group=self.host_group)  # every period-p record precedes any wait
+            self.x, self.x2 = self.x2, self.x
+            self.v, self.v2 = self.v2, self.v
+            k += n
+            p += 1
+        # neighbours' final writes land only in ghost zones; our owned cells are
+        # complete on our stream.  Make sure no peer kernel still targets us.
+        for evs in self.peer_events.values():
+            evs[(p - 1) % 2].wait(main)
 
     # -- ghost exchange ------------------------------------------------------
     def boundary(self, x, v):
@@ -207,6 +324,9 @@ class ShardedChain:
     def run(self, nsteps: int):
         """Advance the shard nsteps steps; returns the 1-based first bad step
         of the WHOLE chain (min over ranks) or 0."""
+        if self.transport == "peer" and self.world > 1 and self.peer_bufs:
+            self._run_peer(nsteps)
+            return self._reduce_first_bad()
         k = 0
         while k < nsteps:
             n = min(self.T, nsteps - k)
@@ -222,6 +342,9 @@ class ShardedChain:
                     self._exchange(self.x, self.v)
             self.phase_edges(n, k)
             k += n
+        return self._reduce_first_bad()
+
+    def _reduce_first_bad(self) -> int:
         fb = self.first_bad.clone()
         if self.world > 1:
             big = torch.iinfo(torch.int64).max
@@ -257,12 +380,41 @@ class LocalShardGroup:
     """
 
     def __init__(self, m, C, x0, v0, dt, shards: int, *, halo_steps=32, device=None,
-                 advance=None):
+                 advance=None, transport="nccl"):
+        self.transport = transport
         self.parts = [ShardedChain(m, C, x0, v0, dt, halo_steps=halo_steps, device=device,
                                    advance=advance, rank=r, world=shards)
                       for r in range(shards)]
+        if transport == "peer":  # neighbours' buffers are plain local tensors here
+            for r, p in enumerate(self.parts):
+                for nb in (r - 1, r + 1):
+                    if 0 <= nb < shards:
+                        q = self.parts[nb]
+                        p.peer_bufs[nb] = (((q.x, q.v), (q.x2, q.v2)), q.L.blo)
+
+    def _run_peer(self, nsteps):
+        """Fused exchange, all shards on one stream: stream order is the only
+        synchronisation needed."""
+        T = self.parts[0].T
+        k = p = 0
+        while k < nsteps:
+            n = min(T, nsteps - k)
+            for sh in self.parts:
+                a, b = sh.L.own
+                left, right = sh.peer_descriptors(p)
+                sh.advance(sh.m, sh.C, sh.x, sh.v, sh.x2, sh.v2, a, b, sh.dt, n, k,
+                           sh.first_bad, left=left, right=right)
+            for sh in self.parts:
+                sh.x, sh.x2 = sh.x2, sh.x
+                sh.v, sh.v2 = sh.v2, sh.v
+            k += n
+            p += 1
 
     def run(self, nsteps: int) -> int:
+        if self.transport == "peer":
+            self._run_peer(nsteps)
+            bad = [int(p.first_bad.item()) for p in self.parts if int(p.first_bad.item()) > 0]
+            return min(bad) if bad else 0
         T = self.parts[0].T
         k = 0
         while k < nsteps:

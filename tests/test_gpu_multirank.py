@@ -35,41 +35,47 @@ def _port():
         return sk.getsockname()[1]
 
 
-def _worker(rank, world, port, s, nsteps, T, stiff, q):
+def _worker(rank, world, port, s, nsteps, T, stiff, transport, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         from paper_1702_02207_b200 import sharded
 
-        sh = sharded.ShardedChain(*_chain(s, 21, stiff), 1e-3, halo_steps=T)
+        sh = sharded.ShardedChain(*_chain(s, 21, stiff), 1e-3, halo_steps=T,
+                                  transport=transport)
         fb = sh.run(nsteps)
         x, v = sh.gather()
+        sh.close()
         if rank == 0:
             q.put((fb, x.numpy(), v.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, s, nsteps, T, stiff=None):
-    return collect(_worker, (world, _port(), s, nsteps, T, stiff), world)
+def _run(world, s, nsteps, T, stiff=None, transport="nccl"):
+    return collect(_worker, (world, _port(), s, nsteps, T, stiff, transport), world)
 
 
-@pytest.mark.parametrize("world,T", [(2, 32), (3, 16)])
-def test_processes_share_a_chain_bit_identically(world, T):
+@pytest.mark.parametrize("world,T,transport", [(2, 32, "nccl"), (3, 16, "nccl"),
+                                               (2, 32, "peer"), (3, 16, "peer")])
+def test_processes_share_a_chain_bit_identically(world, T, transport):
+    """transport="peer": CUDA IPC buffers and interprocess events between the
+    processes; the tile kernel writes the neighbours' ghost zones itself."""
     from paper_1702_02207_b200 import batched
 
     s, n = 200_000, 97
-    fb, x, v = _run(world, s, n, T)
+    fb, x, v = _run(world, s, n, T, transport=transport)
     ref = batched.integrate_chains(*_chain(s, 21), 1e-3, n)
     assert fb == 0
     assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
 
 
-def test_processes_report_first_divergence():
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_processes_report_first_divergence(transport):
     from paper_1702_02207_b200 import batched
 
     s = 60_000
-    fb, _, _ = _run(2, s, 300, 32, stiff=50_000)
+    fb, _, _ = _run(2, s, 300, 32, stiff=50_000, transport=transport)
     ref = batched.integrate_chains(*_chain(s, 21, 50_000), 1e-3, 300, check=False)
     assert fb > 0 and fb == int(ref.first_bad[0])

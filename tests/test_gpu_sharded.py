@@ -58,3 +58,27 @@ def test_local_group_cuda_divergence():
     fb = grp.run(300)
     ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 300, check=False)
     assert fb > 0 and fb == int(ref.first_bad[0])
+
+
+@pytest.mark.parametrize("shards,T", [(2, 32), (3, 16), (8, 32)])
+def test_local_group_peer_transport_bit_identical(shards, T):
+    """Fused compute + exchange: the tile kernel writes its boundary cells into
+    the neighbours' next-input ghost zones."""
+    s = 300_000
+    m, C, x0, v0 = _chain(s, 40 + shards)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, shards, halo_steps=T, transport="peer")
+    assert grp.run(101) == 0
+    x, v = grp.gather()
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 101)
+    assert bits(x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
+    assert bits(v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())
+
+
+def test_local_group_peer_transport_divergence():
+    s = 100_000
+    m, C, x0, v0 = _chain(s, 4)
+    C[60_000] = 1e8
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 4, halo_steps=32, transport="peer")
+    fb = grp.run(300)
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 300, check=False)
+    assert fb > 0 and fb == int(ref.first_bad[0])

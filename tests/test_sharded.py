@@ -123,3 +123,49 @@ def test_local_group_matches_single_chain():
     _, _, xo, vo, _ = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 45,
                                           sample=False)
     assert bits(x.numpy()) == bits(xo[0]) and bits(v.numpy()) == bits(vo[0])
+
+
+def peer_oracle_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
+                        left=None, right=None, **_):
+    """oracle_advance plus the fused exchange: owned boundary cells are also
+    written through the osc_peer_t descriptors (raw host pointers here)."""
+    import ctypes
+
+    oracle_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad)
+    for side, desc in ((0, left), (1, right)):
+        if desc is None:
+            continue
+        px, pv, offset, count = desc
+        lo = own_lo if side == 0 else own_hi - count
+        for ptr, src in ((px, xout), (pv, vout)):
+            arr = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_double)),
+                                        shape=(lo + count + offset,))
+            arr[lo + offset:lo + count + offset] = src[lo:lo + count].numpy()
+
+
+def test_local_group_peer_transport_matches_single_chain():
+    s = 3000
+    m, C, x0, v0 = _chain(s, 6)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 4, halo_steps=6,
+                                  device=torch.device("cpu"), advance=peer_oracle_advance,
+                                  transport="peer")
+    assert grp.run(45) == 0
+    x, v = grp.gather()
+    _, _, xo, vo, _ = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 45,
+                                          sample=False)
+    assert bits(x.numpy()) == bits(xo[0]) and bits(v.numpy()) == bits(vo[0])
+
+
+def test_peer_descriptors_target_next_input_buffers():
+    s = 400
+    m, C, x0, v0 = _chain(s, 1)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 2, halo_steps=4,
+                                  device=torch.device("cpu"), transport="peer")
+    a, b = grp.parts
+    left, right = a.peer_descriptors(0)
+    assert left is None
+    # rank 0's last 8 owned cells land in rank 1's buffer 1 (its next input)
+    assert right[0] == b.x2.data_ptr() and right[3] == 8
+    assert right[2] == a.L.blo - b.L.blo
+    l1, r1 = b.peer_descriptors(1)
+    assert r1 is None and l1[0] == a.x.data_ptr()  # period 1: rank 0 reads buffer 1 next

@@ -124,7 +124,7 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 
 class Workload:
-    def __init__(self, name, rank, device, halo, world=1):
+    def __init__(self, name, rank, device, halo, world=1, transport="nccl"):
         import torch
 
         from paper_1702_02207_b200 import batched
@@ -153,9 +153,9 @@ class Workload:
             self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",
                          "cells": workloads.C3_S, "halo_steps": T,
                          "sharding": f"{world} contiguous shards, 2T-cell ghost zones "
-                                     "exchanged every T steps (NCCL send/recv)"}
+                                     f"refreshed every T steps ({transport})"}
             self.shard = None
-            if world > 1:
+            if world > 1 and transport == "nccl":
                 self.launches = 3 * self.launches  # interior + 2 edge launches per period
         elif name == "C5":
             arrays = workloads.c5(rank=rank)  # m, K, X0, V0
@@ -178,7 +178,8 @@ class Workload:
             from paper_1702_02207_b200 import sharded
 
             # strong scaling: each rank owns s/world cells plus 2T-cell ghosts
-            self.shard = sharded.ShardedChain(*self.dev, self.dt, halo_steps=T, device=device)
+            self.shard = sharded.ShardedChain(*self.dev, self.dt, halo_steps=T, device=device,
+                                              transport=transport)
             lo, hi = self.shard.L.own
             self.shard_x0 = self.shard.x.clone()
             self.shard_v0 = self.shard.v.clone()
@@ -476,6 +477,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--halo", type=int, default=0, help="C3 steps per tiled launch")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="C3 multi-GPU ghost exchange: NCCL P2P, or peer-memory stores "
+                         "fused into the tile kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
@@ -505,7 +509,7 @@ def main():
     if world > 1 and args.config == "C1":
         raise SystemExit("C1 is one serial 2-DOF system: replicas only (DESIGN.md)")
 
-    wl = Workload(args.config, rank, device, args.halo, world)
+    wl = Workload(args.config, rank, device, args.halo, world, args.transport)
     fp64 = fp64_peak(local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > L2 (126 MB)
 
@@ -583,6 +587,8 @@ def main():
                        "mean_ns": st.mean * 1e9, "stddev_ns": st.stddev * 1e9,
                        "timer": "%globaltimer around each step (lane 0)"}
 
+    if getattr(wl, "shard", None) is not None:
+        wl.shard.close()  # collective: every rank releases its peer mappings
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -660,8 +666,6 @@ def main():
     if fma_line:
         line["fma_mode"] = fma_line
     print(json.dumps(line))
-    if getattr(wl, "shard", None) is not None:
-        wl.shard.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

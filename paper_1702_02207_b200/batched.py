@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .oscillator import NonFiniteStateError, accumulated_times
+from .oscillator import NonFiniteStateError, NonPositiveParameterError, accumulated_times
 
 
 def _stream(stream=None) -> int:
@@ -108,6 +108,17 @@ def _outputs(x0, v0, nsteps, stride, sample):
     return x, v, xs, vs
 
 
+def validate_parameters(m, C):
+    """OscillatorSystem's rule (oscillator.py:75-80) for whole batches: every
+    mass and spring rate positive and finite.  One device reduction."""
+    for label, a in (("masses", m), ("springs", C)):
+        bad = ~(torch.isfinite(a) & (a > 0))
+        if bool(bad.any()):
+            idx = tuple(int(i) for i in torch.nonzero(bad)[0])
+            raise NonPositiveParameterError(
+                f"{label}{list(idx)} = {float(a[idx])!r}; must be positive and finite")
+
+
 def _energies(nsteps, stride, B, device, want):
     if not want:
         return None
@@ -115,13 +126,18 @@ def _energies(nsteps, stride, B, device, want):
 
 
 def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
-                     fma=False, stream=None, check=True) -> BatchResult:
-    """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2)."""
+                     fma=False, validate=True, stream=None, check=True) -> BatchResult:
+    """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2).
+
+    ``validate`` applies OscillatorSystem's parameter rule to the batch (one
+    device reduction; pass False when the same arrays were validated before)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
     m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
     if m.dim() != 2 or m.shape[0] != 2 or not (m.shape == C.shape == x0.shape == v0.shape):
         raise ValueError(f"expected [2][B] arrays, got {tuple(m.shape)}")
+    if validate:
+        validate_parameters(m, C)
     B = m.shape[1]
     x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
     es = _energies(nsteps, stride, B, m.device, energies)
@@ -135,7 +151,8 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
 
 
 def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
-                     halo_steps=0, fma=False, stream=None, check=True) -> BatchResult:
+                     halo_steps=0, fma=False, validate=True, stream=None,
+                     check=True) -> BatchResult:
     """B wall-anchored chains of s cells, ``[B][s]`` (oscillator.py:152-263)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
@@ -144,6 +161,8 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
         m, C, x0, v0 = (a[None] for a in (m, C, x0, v0))
     if not (m.shape == C.shape == x0.shape == v0.shape) or m.dim() != 2:
         raise ValueError(f"expected [B][s] arrays, got {tuple(m.shape)}")
+    if validate:
+        validate_parameters(m, C)
     B, s = m.shape
     x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
     es = _energies(nsteps, stride, B, m.device, energies)

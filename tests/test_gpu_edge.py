@@ -121,3 +121,21 @@ def test_many_small_chains_whole_chain_mode():
         res = batched.integrate_chains(m, C, x0, v0, 1e-3, 600)
         _, _, xo, vo, _ = oracle.c_rk4_chains(m, C, x0, v0, 1e-3, 600, sample=False)
         assert bits(res.x.cpu().numpy()) == bits(xo) and bits(res.v.cpu().numpy()) == bits(vo)
+
+
+def test_batch_parameter_validation_mirrors_reference():
+    """OscillatorSystem's rule (oscillator.py:75-80) applied to whole batches."""
+    import paper_1702_02207_b200 as osc
+
+    ok = np.ones((2, 4))
+    for bad in (0.0, -1.0, np.nan, np.inf):
+        m = ok.copy()
+        m[1, 2] = bad
+        with pytest.raises(osc.NonPositiveParameterError):
+            batched.integrate_batch2(m, ok, ok, ok, 1e-3, 5)
+        with pytest.raises(osc.NonPositiveParameterError):
+            batched.integrate_chains(ok, m, ok, ok, 1e-3, 5)
+    # subnormal masses are positive and finite: accepted, as by the reference
+    m = ok.copy()
+    m[0, 0] = 5e-324
+    batched.integrate_batch2(m, ok, ok * 0, ok * 0, 1e-3, 5)

@@ -140,3 +140,44 @@ def test_dense_restatement_tracks_analytic():
     X, V = oracle.dense_rk4(A, X0, V0, 1e-4, 200)
     Xa = oracle.dense_analytic(m, K, X0, 200 * 1e-4)
     assert np.max(np.abs(X - Xa)) <= 1e-8 * np.max(np.abs(X0))
+
+
+# --------------------------------------------------------------------------
+# property-based parity against the reference itself (build container only:
+# the reference package is not on the GPU box)
+# --------------------------------------------------------------------------
+
+import os  # noqa: E402
+import sys  # noqa: E402
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_REF = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(_REF), reason="reference package not present")
+@settings(max_examples=40, deadline=None)
+@given(s=st.integers(1, 9), nsteps=st.integers(1, 60), stride=st.integers(1, 7),
+       seed=st.integers(0, 2**32 - 1), dt=st.sampled_from([1e-4, 1e-3, 5e-3, 2e-2]))
+def test_c_oracle_equals_reference_on_random_chains(s, nsteps, stride, seed, dt):
+    sys.path.insert(0, _REF)
+    import oscbench
+
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(0.3, 3.0, s)
+    C = rng.uniform(100.0, 3000.0, s)
+    x0 = rng.standard_normal(s) * rng.choice([1e-3, 1.0, 1e3])
+    v0 = rng.standard_normal(s)
+    x0[rng.random(s) < 0.2] = 0.0
+    try:
+        traj = oscbench.integrate(oscbench.build_chain(m, C), oscbench.PhaseState(x0, v0),
+                                  dt, nsteps, stride)
+        ref_bad = 0
+    except oscbench.NonFiniteStateError as exc:
+        ref_bad = exc.step
+    xs, vs, _, _, fb = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], dt, nsteps,
+                                           stride)
+    assert fb[0] == ref_bad
+    if not ref_bad:
+        assert bits(xs[:, 0]) == bits(np.array([p.positions for p in traj.samples]))
+        assert bits(vs[:, 0]) == bits(np.array([p.velocities for p in traj.samples]))

@@ -9,7 +9,9 @@
  * build:  gcc -O2 -I include examples/c_abi_demo.c -o c_abi_demo \
  *           -L paper_1702_02207_b200 -l:libosc_b200.so -L/usr/local/cuda/lib64 -lcudart \
  *           -Wl,-rpath,$PWD/paper_1702_02207_b200
- * run:    ./c_abi_demo   (prints "ok" and exits 0)
+ * run:    ./c_abi_demo [dump.bin]   (prints "ok" and exits 0; with a path, also
+ *         writes m, C, x0, v0, x, v as raw float64 [2][B] each, so a checker can
+ *         compare the result with the CPU oracle)
  */
 #include <math.h>
 #include <stdint.h>
@@ -30,9 +32,10 @@ static double urand(uint64_t *s)
     return (double)(*s >> 11) * (1.0 / 9007199254740992.0);
 }
 
-int main(void)
+int main(int argc, char **argv)
 {
-    static double m[2 * B], C[2 * B], x[2 * B], v[2 * B], x2[2 * B], v2[2 * B];
+    static double m[2 * B], C[2 * B], x[2 * B], v[2 * B], x2[2 * B], v2[2 * B], x0[2 * B],
+        v0[2 * B];
     static int64_t fb[B], fb2[B];
     uint64_t seed = 1702;
     for (int i = 0; i < 2 * B; ++i) {
@@ -41,6 +44,8 @@ int main(void)
         x[i] = 2.0 * urand(&seed) - 1.0;
         v[i] = 0.0;
     }
+    memcpy(x0, x, sizeof x);
+    memcpy(v0, v, sizeof v);
     memcpy(x2, x, sizeof x);
     memcpy(v2, v, sizeof v);
 
@@ -87,6 +92,21 @@ int main(void)
             fprintf(stderr, "non-finite state\n");
             return 1;
         }
+
+    if (argc > 1) {
+        FILE *f = fopen(argv[1], "wb");
+        if (!f) {
+            perror(argv[1]);
+            return 1;
+        }
+        fwrite(m, sizeof m, 1, f);
+        fwrite(C, sizeof C, 1, f);
+        fwrite(x0, sizeof x0, 1, f);
+        fwrite(v0, sizeof v0, 1, f);
+        fwrite(x, sizeof x, 1, f);
+        fwrite(v, sizeof v, 1, f);
+        fclose(f);
+    }
 
     /* 3. the error contract */
     if (osc_rk4_batch2_host(m, C, x, v, B, -1.0, 10, 1, NULL, NULL, fb) != OSC_INVALID) {

@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 4
+#define OSC_ABI_VERSION 5
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -68,6 +68,32 @@ const char *osc_last_error(void);
 int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                    double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
                    double *es, int64_t *first_bad, uint32_t flags, void *stream);
+
+/* Numeric-vs-analytic validation of 2-DOF batches on the device (the
+ * reference's modal.py, batched).  Solution records are SoA [8][B] in the
+ * order omega1, omega2, r1, r2, a1c, a1s, a2c, a2s (Analytic2DOF,
+ * modal.py:44-62); reports are [3][B]: max_abs_error, rmse, at_time
+ * (ErrorReport, modal.py:65-71).
+ * osc_analytic_batch2: analytic_solution (modal.py:98-120) per system;
+ *   bit-identical to the reference for equal parameters (m0 == m1, C0 == C1),
+ *   the same modal construction for the general 2x2 pencil otherwise.
+ *   Parameters are not validated here (callers validate as
+ *   OscillatorSystem does).
+ * osc_compare_batch2: compare (modal.py:141-162) of nsamp retained samples,
+ *   xs [nsamp][2][B] with time labels ts [nsamp]; OSC_INVALID if nsamp < 1.
+ * osc_rk4_batch2_compare: osc_rk4_batch2 with compare() accumulated in the
+ *   time loop at every retained sample (ts: the 1 + nsteps/stride labels)
+ *   and no samples written; a diverged system's report is NaN.
+ * eval_analytic's cos/sin are CUDA's (<= 2 ulp), so reports match the
+ * reference to a tolerance, not bit for bit. */
+int osc_analytic_batch2(const double *m, const double *C, const double *x0, const double *v0,
+                        int64_t B, double *sol, void *stream);
+int osc_compare_batch2(const double *sol, const double *xs, const double *ts, int64_t nsamp,
+                       int64_t B, double *report, void *stream);
+int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *v, int64_t B,
+                           double dt, int64_t nsteps, int64_t stride, const double *ts,
+                           const double *sol, double *report, int64_t *first_bad, uint32_t flags,
+                           void *stream);
 
 /* B independent wall-anchored chains of s cells, layout [B][s]
  * (spring i joins cell i to cell i-1, spring 0 to the wall, last cell free;

@@ -281,6 +281,51 @@ def compare(times, xs, sol):
     return float(flat[j]), float(math.sqrt(np.mean(flat * flat))), float(times[j // 2])
 
 
+def compare_seq(times, xs, sol):
+    """modal.py:141-162 literally: samples in order, both coordinates,
+    sequential sum of squares, strict ``>`` for the maximum.  math.cos/sin
+    (glibc) as in the reference.  -> (max_abs_error, rmse, at_time)."""
+    w1, w2, r1, r2, a1c, a1s, a2c, a2s = (float(f) for f in sol)
+    max_err, at_time, sum_sq, count = -1.0, 0.0, 0.0, 0
+    for t, (p0, p1) in zip(times, xs):
+        t = float(t)
+        mode1 = a1c * math.cos(w1 * t) + a1s * math.sin(w1 * t)
+        mode2 = a2c * math.cos(w2 * t) + a2s * math.sin(w2 * t)
+        for num, ana in ((float(p0), mode1 + mode2), (float(p1), r1 * mode1 + r2 * mode2)):
+            err = abs(num - ana)
+            sum_sq += err * err
+            count += 1
+            if err > max_err:
+                max_err, at_time = err, t
+    return max_err, math.sqrt(sum_sq / count), at_time
+
+
+def analytic_general(m0, m1, C0, C1, x0, v0):
+    """Two-mode solution of a 2-DOF wall-anchored chain with arbitrary
+    parameters: analytic_solution (modal.py:98-120) when m0 == m1 and
+    C0 == C1, else the same modal construction for K - w^2 M with
+    K = [[C0 + C1, -C1], [-C1, C1]], M = diag(m0, m1) -- operation for
+    operation what osc_modal.cuh computes (outside the reference)."""
+    if m0 == m1 and C0 == C1:
+        return analytic_solution(m0, C0, x0, v0)
+    a = m0 * m1
+    b = m0 * C1 + m1 * (C0 + C1)
+    c = C0 * C1
+    disc = b * b - 4.0 * (a * c)
+    q = b + math.sqrt(disc if disc > 0.0 else 0.0)
+    L1 = q / (2.0 * a)
+    L2 = (2.0 * c) / q
+    w1, w2 = math.sqrt(L1), math.sqrt(L2)
+    r1 = C1 / (C1 - L1 * m1)
+    r2 = C1 / (C1 - L2 * m1)
+    det = r2 - r1
+    a1c = (r2 * x0[0] - x0[1]) / det
+    a2c = (x0[1] - r1 * x0[0]) / det
+    u1 = (r2 * v0[0] - v0[1]) / det
+    u2 = (v0[1] - r1 * v0[0]) / det
+    return (w1, w2, r1, r2, a1c, u1 / w1, a2c, u2 / w2)
+
+
 # --------------------------------------------------------------------------
 # dense general-(M,K) restatement (SPEC.md:8/188 -- outside the reference)
 # --------------------------------------------------------------------------

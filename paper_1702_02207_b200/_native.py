@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
-ABI_VERSION = 4
+ABI_VERSION = 5
 OSC_FMA = 1
 
 _i64 = ctypes.c_int64
@@ -27,6 +27,10 @@ SIGNATURES = {
     "osc_last_error": (ctypes.c_char_p, []),
     "osc_rk4_batch2": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp, _vp,
                                       _vp, _vp, ctypes.c_uint32, _vp]),
+    "osc_analytic_batch2": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "osc_compare_batch2": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp]),
+    "osc_rk4_batch2_compare": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,
+                                              _vp, _vp, _vp, ctypes.c_uint32, _vp]),
     "osc_rk4_chains": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64, _vp,
                                       _vp, _vp, _vp, _i64, ctypes.c_uint32, _vp]),
     "osc_rk4_chain_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,

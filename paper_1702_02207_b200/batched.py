@@ -5,7 +5,10 @@ CUDA tensors (used in place when contiguous).  Work is enqueued on the current
 torch stream; results are device tensors.  These are the calls the bench and
 the multi-GPU driver make; ``oscillator.integrate`` is the drop-in wrapper.
 
-    integrate_batch2   BASELINE configs 0-1  (K1 batch2_rk4)
+    integrate_batch2   BASELINE configs 0-1  (K1 batch2_rk4; compare=True fuses
+                       modal.compare against the analytic solution)
+    analytic_batch2    modal.analytic_solution per system
+    compare_batch2     modal.compare over retained samples
     integrate_chains   BASELINE configs 2-3  (K2 whole-chain / K3 tiled)
     chain_advance      one temporally blocked launch over a shard (K3)
 """
@@ -71,6 +74,7 @@ class BatchResult:
     stride: int
     t0: float = 0.0
     energies: torch.Tensor | None = None  # [nsamp][B] energy() of each sample
+    errors: "ErrorReports | None" = None  # compare() vs the analytic solution
 
     def energy_drift(self) -> torch.Tensor:
         """max_k |E_k - E_0| / E_0 per system (harness.py:508-510's drift)."""
@@ -95,6 +99,57 @@ class BatchResult:
             raise NonFiniteStateError(
                 f"integration diverged at step {step} (system {idx})", step=step)
         return self
+
+
+@dataclass
+class ErrorReports:
+    """modal.ErrorReport (modal.py:65-71) for every system of a batch, [B]
+    each; NaN for a system that diverged (integrate would have raised)."""
+
+    max_abs_error: torch.Tensor
+    rmse: torch.Tensor
+    at_time: torch.Tensor
+
+
+MODAL_FIELDS = ("omega1", "omega2", "r1", "r2", "a1c", "a1s", "a2c", "a2s")
+
+
+def analytic_batch2(m, C, x0, v0, *, stream=None) -> torch.Tensor:
+    """modal.analytic_solution (modal.py:98-120) per system, ``[8][B]`` in
+    MODAL_FIELDS order.  Equal parameters give the reference's bits; unequal
+    ones the general two-mode solution of the 2x2 pencil (osc_modal.cuh)."""
+    lib = _native.lib()
+    m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
+    if m.dim() != 2 or m.shape[0] != 2 or not (m.shape == C.shape == x0.shape == v0.shape):
+        raise ValueError(f"expected [2][B] arrays, got {tuple(m.shape)}")
+    validate_parameters(m, C)
+    B = m.shape[1]
+    sol = torch.empty((len(MODAL_FIELDS), B), dtype=torch.float64, device=m.device)
+    rc = lib.osc_analytic_batch2(_ptr(m), _ptr(C), _ptr(x0), _ptr(v0), B, _ptr(sol),
+                                 ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_analytic_batch2")
+    return sol
+
+
+def _reports(out: torch.Tensor) -> ErrorReports:
+    return ErrorReports(out[0], out[1], out[2])
+
+
+def compare_batch2(sol, xs, ts, *, stream=None) -> ErrorReports:
+    """modal.compare (modal.py:141-162) of retained samples ``xs``
+    ``[nsamp][2][B]`` at time labels ``ts`` against ``sol`` ``[8][B]``."""
+    lib = _native.lib()
+    sol, xs, ts = _dev(sol), _dev(xs), _dev(ts)
+    if xs.dim() != 3 or xs.shape[1] != 2 or ts.shape != (xs.shape[0],):
+        raise ValueError("expected xs [nsamp][2][B] and ts [nsamp]")
+    B = xs.shape[2]
+    if sol.shape != (len(MODAL_FIELDS), B):
+        raise ValueError(f"expected sol [8][{B}], got {tuple(sol.shape)}")
+    out = torch.empty((3, B), dtype=torch.float64, device=xs.device)
+    rc = lib.osc_compare_batch2(_ptr(sol), _ptr(xs), _ptr(ts), xs.shape[0], B, _ptr(out),
+                                ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_compare_batch2")
+    return _reports(out)
 
 
 def _outputs(x0, v0, nsteps, stride, sample):
@@ -126,11 +181,16 @@ def _energies(nsteps, stride, B, device, want):
 
 
 def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
-                     fma=False, validate=True, stream=None, check=True) -> BatchResult:
+                     compare=False, analytic=None, fma=False, validate=True, stream=None,
+                     check=True) -> BatchResult:
     """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2).
 
     ``validate`` applies OscillatorSystem's parameter rule to the batch (one
-    device reduction; pass False when the same arrays were validated before)."""
+    device reduction; pass False when the same arrays were validated before).
+    ``compare``: also return ``errors``, modal.compare of every retained
+    sample against the analytic solution (``analytic``: a precomputed
+    ``analytic_batch2`` result).  Without samples or energies the error is
+    accumulated inside the time loop and no sample is written."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
     m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
@@ -139,14 +199,36 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
     if validate:
         validate_parameters(m, C)
     B = m.shape[1]
-    x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
-    es = _energies(nsteps, stride, B, m.device, energies)
+    flags = _native.OSC_FMA if fma else 0
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
-    rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt), int(nsteps),
-                            int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb),
-                            _native.OSC_FMA if fma else 0, ctypes.c_void_p(_stream(stream)))
-    raise_for(rc, "osc_rk4_batch2")
-    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es)
+    errors = None
+    if compare:
+        sol = _dev(analytic) if analytic is not None else analytic_batch2(m, C, x0, v0,
+                                                                         stream=stream)
+        ts = _dev(accumulated_times(0.0, float(dt), int(nsteps), int(stride)))
+    if compare and not (sample or energies):
+        x, v = x0.clone(), v0.clone()
+        xs = vs = es = None
+        out = torch.empty((3, B), dtype=torch.float64, device=m.device)
+        rc = lib.osc_rk4_batch2_compare(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt),
+                                        int(nsteps), int(stride), _ptr(ts), _ptr(sol), _ptr(out),
+                                        _ptr(fb), flags, ctypes.c_void_p(_stream(stream)))
+        raise_for(rc, "osc_rk4_batch2_compare")
+        errors = _reports(out)
+    else:
+        x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample or compare)
+        es = _energies(nsteps, stride, B, m.device, energies)
+        rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt), int(nsteps),
+                                int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb), flags,
+                                ctypes.c_void_p(_stream(stream)))
+        raise_for(rc, "osc_rk4_batch2")
+        if compare:
+            errors = compare_batch2(sol, xs, ts, stream=stream)
+            bad = fb > 0
+            for t in (errors.max_abs_error, errors.rmse, errors.at_time):
+                t.masked_fill_(bad, float("nan"))
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es,
+                      errors=errors)
     return res.check() if check else res
 
 

@@ -154,6 +154,58 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "batch2_rk4_kernel");
 }
 
+int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *v, int64_t B,
+                           double dt, int64_t nsteps, int64_t stride, const double *ts,
+                           const double *sol, double *report, int64_t *first_bad, uint32_t flags,
+                           void *stream)
+{
+    if (flags & ~uint32_t(OSC_FMA))
+        return fail(OSC_INVALID, "unknown flags 0x%x", flags);
+    if (int rc = check_run_args(dt, nsteps, stride))
+        return rc;
+    if (B < 0)
+        return fail(OSC_INVALID, "B must be >= 0");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x || !v || !first_bad || !ts || !sol || !report)
+        return fail(OSC_INVALID, "null buffer");
+    const osc::CmpArgs cmp{ts, sol, report};
+    cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, nullptr, nullptr,
+                                       nullptr, first_bad, (flags & OSC_FMA) != 0,
+                                       static_cast<cudaStream_t>(stream), &cmp);
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "batch2_rk4_kernel<compare>");
+}
+
+int osc_analytic_batch2(const double *m, const double *C, const double *x0, const double *v0,
+                        int64_t B, double *sol, void *stream)
+{
+    if (B < 0)
+        return fail(OSC_INVALID, "B must be >= 0");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x0 || !v0 || !sol)
+        return fail(OSC_INVALID, "null buffer");
+    cudaError_t e = osc::launch_modal_batch2(m, C, x0, v0, B, sol,
+                                             static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "modal_batch2_kernel");
+}
+
+int osc_compare_batch2(const double *sol, const double *xs, const double *ts, int64_t nsamp,
+                       int64_t B, double *report, void *stream)
+{
+    if (B < 0)
+        return fail(OSC_INVALID, "B must be >= 0");
+    if (nsamp < 1)
+        return fail(OSC_INVALID, "empty trajectory");  // modal.py:143-144
+    if (B == 0)
+        return OSC_OK;
+    if (!sol || !xs || !ts || !report)
+        return fail(OSC_INVALID, "null buffer");
+    cudaError_t e = osc::launch_compare_batch2(sol, xs, ts, nsamp, B, report,
+                                               static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "compare_batch2_kernel");
+}
+
 int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64_t B, int64_t s,
                    double dt, int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
                    int64_t *first_bad, int64_t halo_steps, uint32_t flags, void *stream_)

@@ -13,6 +13,7 @@
 // (-C)*d == -(C*d) exactly under round-to-nearest, so f1 = C1*d1 is shared.
 #include "osc_device.cuh"
 #include "osc_kernels.h"
+#include "osc_modal.cuh"
 
 #include <cstdio>
 #include <cstdlib>
@@ -110,14 +111,15 @@ constexpr int kChunk = 64;  // steps between divergence checks
 // NS systems per thread, interleaved for instruction-level parallelism:
 // system j of thread t in block b is b*NS*blockDim + j*blockDim + t, so each
 // load/store of a warp stays one contiguous 256 B run.  Indices past B
-// duplicate the last system and are never stored.
-template <int NS, bool kFma>
+// duplicate the last system and are never stored.  kCmp: also accumulate
+// compare() against the analytic solution at every retained sample.
+template <int NS, bool kFma, bool kCmp = false>
 __global__ void __launch_bounds__(256)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
                   StepConsts k, int64_t nsteps, int64_t stride, double *__restrict__ xs,
                   double *__restrict__ vs, double *__restrict__ es,
-                  int64_t *__restrict__ first_bad)
+                  int64_t *__restrict__ first_bad, CmpArgs cmp = CmpArgs{})
 {
     const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * NS + threadIdx.x;
     int64_t idx[NS];
@@ -146,6 +148,12 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         }
         if (es && live[j])
             es[i] = energy2(s[j], m[i], m[B + i], C0[j], C1[j]);
+    }
+    ErrAcc acc[kCmp ? NS : 1];
+    if constexpr (kCmp) {
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+            acc[j].add_sample(load_modal(cmp.sol, B, idx[j]), cmp.ts[0], s[j].x0, s[j].x1);
     }
     int64_t bad[NS];
 #pragma unroll
@@ -214,6 +222,15 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                 }
             }
         }
+        if constexpr (kCmp) {
+            if (kstep % stride == 0) {
+#pragma unroll
+                for (int j = 0; j < NS; ++j)
+                    if (bad[j] == 0)
+                        acc[j].add_sample(load_modal(cmp.sol, B, idx[j]), cmp.ts[kstep / stride],
+                                          s[j].x0, s[j].x1);
+            }
+        }
         bool all_bad = true;
 #pragma unroll
         for (int j = 0; j < NS; ++j)
@@ -230,6 +247,12 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             v[i] = s[j].v0;
             v[B + i] = s[j].v1;
             first_bad[i] = bad[j];
+            if constexpr (kCmp) {
+                const double nan = __longlong_as_double(0x7ff8000000000000ll);
+                cmp.out[i] = bad[j] ? nan : acc[j].max_err;
+                cmp.out[B + i] = bad[j] ? nan : acc[j].rmse();
+                cmp.out[2 * B + i] = bad[j] ? nan : acc[j].at_time;
+            }
         }
     }
 }
@@ -238,11 +261,18 @@ template <int NS>
 cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, int64_t B,
                       StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
                       double *es, int64_t *first_bad, int threads, bool fma,
-                      cudaStream_t stream)
+                      cudaStream_t stream, const CmpArgs *cmp)
 {
     const int64_t per_block = int64_t(threads) * NS;
     const unsigned blocks = static_cast<unsigned>((B + per_block - 1) / per_block);
-    if (fma)
+    if (cmp) {
+        if (fma)
+            batch2_rk4_kernel<NS, true, true><<<blocks, threads, 0, stream>>>(
+                m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, *cmp);
+        else
+            batch2_rk4_kernel<NS, false, true><<<blocks, threads, 0, stream>>>(
+                m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, *cmp);
+    } else if (fma)
         batch2_rk4_kernel<NS, true><<<blocks, threads, 0, stream>>>(
             m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
     else
@@ -255,7 +285,8 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
 
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                          double *es, int64_t *first_bad, bool fma, cudaStream_t stream)
+                          double *es, int64_t *first_bad, bool fma, cudaStream_t stream,
+                          const CmpArgs *cmp)
 {
     // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
     // overrides it for benchmarking (read-only process state).
@@ -276,9 +307,9 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
         }
     }
     switch (ns) {
-    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream);
-    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream);
-    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream);
+    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp);
+    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp);
+    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp);
     }
 }
 

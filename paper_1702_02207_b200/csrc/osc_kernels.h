@@ -33,9 +33,25 @@ struct SegArgs {
     PeerGhost peer[2];       // left / right neighbour ghost targets (x == nullptr: none)
 };
 
+// Fused compare (modal.py:141-162) at every retained sample of K1: ts are
+// the samples' time labels, sol the [8][B] analytic solutions, out the
+// [3][B] ErrorReport fields (max_err, rmse, at_time; NaN if diverged).
+struct CmpArgs {
+    const double *ts;
+    const double *sol;
+    double *out;
+};
+
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
-                          double *es, int64_t *first_bad, bool fma, cudaStream_t stream);
+                          double *es, int64_t *first_bad, bool fma, cudaStream_t stream,
+                          const CmpArgs *cmp = nullptr);
+
+cudaError_t launch_modal_batch2(const double *m, const double *C, const double *x0,
+                                const double *v0, int64_t B, double *sol, cudaStream_t stream);
+
+cudaError_t launch_compare_batch2(const double *sol, const double *xs, const double *ts,
+                                  int64_t nsamp, int64_t B, double *out, cudaStream_t stream);
 
 cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream);
 

@@ -2,7 +2,7 @@
 
 Run in the build container (the reference does not exist on the GPU box):
 
-    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/gen_golden.py
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/gen_golden.py [modal]
 
 Every fixture is the output of ``oscbench.integrate`` / ``oscbench.energy`` /
 ``oscbench.derivative`` (oscillator.py:184-276) on the inputs stored beside it,
@@ -141,8 +141,45 @@ def main():
     edge["chain3_energy"] = np.float64(oscbench.energy(sys3, st3))
     save("edge", **edge)
 
+    modal_fixture()
     print(f"done in {time.time() - t_start:.1f} s")
 
 
+def modal_fixture():
+    """modal.analytic_solution + integrate + modal.compare (modal.py:98-162)
+    on equal-parameter systems: the paper's C1 system, the canonical test
+    system and seeded random ones (m, C, x0, v0 all varied, v0 != 0)."""
+    from oscbench import modal
+
+    rng = np.random.default_rng(1702)
+    cases = [(1.0, 1012.5, (1.0, 0.0), (0.0, 0.0)),
+             (0.002, 20250.0, (2.0, -3.0), (0.0, 0.0))]
+    for _ in range(14):
+        cases.append((float(rng.uniform(0.5, 2.0)), float(rng.uniform(500.0, 2000.0)),
+                      tuple(float(a) for a in rng.standard_normal(2)),
+                      tuple(float(a) for a in rng.standard_normal(2) * 10.0)))
+    # (dt, nsteps, stride) per case: C1 a shortened paper run, canonical the
+    # reference tests' config, the random ones 2000 steps at omega*dt <= 0.1
+    runs = [(1e-4, 100_000, 100), (1e-6, 10_000, 100)] + [(1e-3, 2000, 10)] * 14
+    sol, rep, xs_all, ts_all = [], [], [], []
+    for (m, c, x0, v0), (dt, n, stride) in zip(cases, runs):
+        a = modal.analytic_solution(m, c, x0, v0)
+        sol.append([a.omega1, a.omega2, a.r1, a.r2, a.a1c, a.a1s, a.a2c, a.a2s])
+        traj = integrate(build_chain([m, m], [c, c]), PhaseState(x0, v0), dt, n, stride)
+        r = modal.compare(traj, a)
+        rep.append([r.max_abs_error, r.rmse, r.at_time])
+        xs_all.append(np.array([s.positions for s in traj.samples]))
+        ts_all.append(np.array(traj.times()))
+    # the random cases share one shape: stack them as one [nsamp][2][B] batch
+    save("modal", m=np.array([c[0] for c in cases]), C=np.array([c[1] for c in cases]),
+         x0=np.array([c[2] for c in cases]), v0=np.array([c[3] for c in cases]),
+         run=np.array(runs, dtype=np.float64), sol=np.array(sol), report=np.array(rep),
+         c1_xs=xs_all[0], c1_ts=ts_all[0], canon_xs=xs_all[1], canon_ts=ts_all[1],
+         rand_xs=np.stack(xs_all[2:], -1), rand_ts=ts_all[2])
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["modal"]:
+        modal_fixture()
+    else:
+        main()

@@ -181,3 +181,51 @@ def test_c_oracle_equals_reference_on_random_chains(s, nsteps, stride, seed, dt)
     if not ref_bad:
         assert bits(xs[:, 0]) == bits(np.array([p.positions for p in traj.samples]))
         assert bits(vs[:, 0]) == bits(np.array([p.velocities for p in traj.samples]))
+
+
+# --------------------------------------------------------------------------
+# modal analytic solution and compare (modal.py:98-162), pinned to
+# tests/golden/modal.npz (the reference's own analytic_solution / compare)
+# --------------------------------------------------------------------------
+
+def test_modal_restatement_matches_reference(golden):
+    g = golden("modal")
+    for i in range(len(g["m"])):
+        sol = oracle.analytic_solution(g["m"][i], g["C"][i], g["x0"][i], g["v0"][i])
+        assert bits(np.array(sol)) == bits(g["sol"][i]), i
+        gen = oracle.analytic_general(g["m"][i], g["m"][i], g["C"][i], g["C"][i], g["x0"][i],
+                                      g["v0"][i])
+        assert bits(np.array(gen)) == bits(g["sol"][i]), i
+
+
+def test_compare_restatement_matches_reference(golden):
+    g = golden("modal")
+    rep = g["report"]
+    assert bits(np.array(oracle.compare_seq(g["c1_ts"], g["c1_xs"], g["sol"][0]))) == bits(rep[0])
+    assert bits(np.array(oracle.compare_seq(g["canon_ts"], g["canon_xs"],
+                                            g["sol"][1]))) == bits(rep[1])
+    for b in range(g["rand_xs"].shape[-1]):
+        got = oracle.compare_seq(g["rand_ts"], g["rand_xs"][:, :, b], g["sol"][2 + b])
+        assert bits(np.array(got)) == bits(rep[2 + b]), b
+
+
+def test_general_modal_solution_is_the_exact_solution():
+    """Unequal parameters (outside modal.py): each mode solves the pencil,
+    and the fit reproduces the initial positions and velocities."""
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        m0, m1 = rng.uniform(0.5, 2.0, 2)
+        C0, C1 = rng.uniform(500.0, 2000.0, 2)
+        x0, v0 = rng.standard_normal(2), rng.standard_normal(2) * 10
+        w1, w2, r1, r2, a1c, a1s, a2c, a2s = oracle.analytic_general(m0, m1, C0, C1, x0, v0)
+        K = np.array([[C0 + C1, -C1], [-C1, C1]])
+        M = np.diag([m0, m1])
+        lam = np.sort(np.linalg.eigvals(np.linalg.solve(M, K)).real)[::-1]
+        assert np.allclose([w1 * w1, w2 * w2], lam, rtol=1e-12)
+        for w, r in ((w1, r1), (w2, r2)):
+            res = (K - w * w * M) @ np.array([1.0, r])
+            assert np.abs(res).max() <= 1e-9 * np.abs(K).max() * (1 + abs(r))
+        x1a, x2a = oracle.eval_analytic((w1, w2, r1, r2, a1c, a1s, a2c, a2s), [0.0])
+        assert np.allclose([x1a[0], x2a[0]], x0, atol=1e-13)
+        vel0 = np.array([w1 * a1s + w2 * a2s, r1 * w1 * a1s + r2 * w2 * a2s])
+        assert np.allclose(vel0, v0, atol=1e-11)

@@ -418,6 +418,22 @@ def cpu_baseline(wl: Workload, budget_s: float = 12.0):
 
 # --------------------------------------------------------------------------
 
+def time_side(fn, warm=2, reps=3) -> float:
+    """Seconds per call of a side measurement (CUDA events, current stream)."""
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e-3 / reps
+
+
 def allreduce_max(value: float, device, backend: str) -> float:
     """Max over ranks (device times are taken per rank; the job's is the max)."""
     import torch
@@ -560,20 +576,30 @@ def main():
     if wl.name in ("C2", "C3", "C4") and world == 1:
         # the opt-in OSC_FMA arithmetic on the same workload (not bit-identical;
         # tolerance in DESIGN.md), for context beside the exact headline
-        fstep = wl.fma_step()
-        for _ in range(2):
-            fstep()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(3):
-            fstep()
-        b.record()
-        torch.cuda.synchronize()
-        fs = a.elapsed_time(b) * 1e-3 / 3
+        fs = time_side(wl.fma_step())
         fma_line = {"value": wl.dof_steps / fs, "unit": UNIT, "ms_per_step": fs * 1e3,
                     "arithmetic": "OSC_FMA: contracted a*b+c, x/m as x*(1/m); rel. error "
                                   "<= 1e-12 vs the reference after 1e4 steps (measured 7e-15)"}
+
+    validation_line = None
+    if wl.name in ("C1", "C2") and world == 1:
+        # On-device validation of every system against its analytic two-mode
+        # solution (modal.compare fused into the K1 time loop).
+        m, C, x0, v0 = wl.dev
+        stride = workloads.PARAMS[wl.name].stride if wl.name == "C1" else 1000
+        sol = wl.batched.analytic_batch2(m, C, x0, v0)
+        run = lambda: wl.batched.integrate_batch2(  # noqa: E731
+            m, C, x0, v0, wl.dt, wl.nsteps, stride, compare=True, analytic=sol, check=False,
+            validate=False)
+        vs = time_side(run)
+        err = run().errors
+        validation_line = {
+            "value": wl.dof_steps / vs, "unit": UNIT, "ms_per_step": vs * 1e3,
+            "samples_per_system": 1 + wl.nsteps // stride,
+            "max_abs_error_max": float(err.max_abs_error.max()),
+            "rmse_max": float(err.rmse.max()),
+            "what": "modal.compare of every system vs its analytic solution, accumulated in "
+                    "the time loop (no samples written)"}
 
     engine_line = None
     if wl.name == "C1":
@@ -669,6 +695,8 @@ def main():
         line["equation_engine"] = engine_line
     if fma_line:
         line["fma_mode"] = fma_line
+    if validation_line:
+        line["validation"] = validation_line
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

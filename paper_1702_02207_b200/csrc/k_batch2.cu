@@ -113,8 +113,8 @@ constexpr int kChunk = 64;  // steps between divergence checks
 // load/store of a warp stays one contiguous 256 B run.  Indices past B
 // duplicate the last system and are never stored.  kCmp: also accumulate
 // compare() against the analytic solution at every retained sample.
-template <int NS, bool kFma, bool kCmp = false>
-__global__ void __launch_bounds__(256)
+template <int NS, bool kFma, bool kCmp = false, int kMaxThreads = 256>
+__global__ void __launch_bounds__(kMaxThreads)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
                   StepConsts k, int64_t nsteps, int64_t stride, double *__restrict__ xs,
@@ -265,6 +265,14 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
 {
     const int64_t per_block = int64_t(threads) * NS;
     const unsigned blocks = static_cast<unsigned>((B + per_block - 1) / per_block);
+    if (NS == 1 && !cmp && !fma && threads == 32) {
+        // Latency path (few systems, e.g. C1): the 32-thread bound gives ptxas
+        // a register budget whose schedule of the serial step is ~12% shorter
+        // (profiles/r01/c1_latency.md).
+        batch2_rk4_kernel<1, false, false, 32><<<blocks, threads, 0, stream>>>(
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
+        return cudaGetLastError();
+    }
     if (cmp) {
         if (fma)
             batch2_rk4_kernel<NS, true, true><<<blocks, threads, 0, stream>>>(
@@ -298,6 +306,8 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (B < int64_t(sms) * 1024)
         ns = 1;
+    if (B <= int64_t(sms) * 32)
+        threads = 32;  // at most one warp per SM anyway: the latency build
     if (const char *e = std::getenv("OSC_B2")) {
         int a = 0, b = 0;
         if (std::sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && b >= 32 &&

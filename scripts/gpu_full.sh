@@ -7,3 +7,7 @@ tail -3 gpurun_out/pytest_gpu.log
 for c in C2 C4 C3 C1; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo bench $c rc=$?; done
 timeout 900 python bench.py --config C5 --steps 2 --warmup 3 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo bench C5 rc=$?
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
+# the driver's multi-rank launch path with the NCCL backend (one rank on one GPU)
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+  --master-port 29533 bench.py --gpus 1 --steps 3 --warmup 3 > gpurun_out/bench_torchrun1.json \
+  2> gpurun_out/bench_torchrun1.err; echo torchrun rc=$?

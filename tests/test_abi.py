@@ -63,6 +63,25 @@ def test_argument_errors_need_no_device(lib):
     assert b"flags" in lib.osc_last_error()
     assert lib.osc_rk4_chain_advance(None, None, None, None, None, None, 100, 0, 100, 1e-3, 600,
                                      0, None, None, None, 0, None) == _native.OSC_INVALID
+    # validation entry points (modal.py): compare of an empty trajectory is
+    # the reference's ValueError("empty trajectory") (modal.py:143-144)
+    assert lib.osc_compare_batch2(None, None, None, 0, 4, None, None) == _native.OSC_INVALID
+    assert b"empty trajectory" in lib.osc_last_error()
+    assert lib.osc_compare_batch2(None, None, None, 3, 4, None, None) == _native.OSC_INVALID
+    assert b"null buffer" in lib.osc_last_error()
+    assert lib.osc_analytic_batch2(None, None, None, None, -1, None, None) == _native.OSC_INVALID
+    assert lib.osc_analytic_batch2(None, None, None, None, 0, None, None) == _native.OSC_OK
+    assert lib.osc_rk4_batch2_compare(None, None, None, None, 4, 1e-3, 10, 0, None, None, None,
+                                      None, 0, None) == _native.OSC_INVALID
+    assert b"stride" in lib.osc_last_error()
+    assert lib.osc_rk4_batch2_compare(None, None, None, None, 4, 1e-3, 10, 1, None, None, None,
+                                      None, 0, None) == _native.OSC_INVALID
+    assert b"null buffer" in lib.osc_last_error()
+    # dense and engine paths check shapes before touching the device
+    assert lib.osc_rk4_dense(None, None, None, 0, 4, 1e-3, 10, None, None) == _native.OSC_INVALID
+    assert lib.osc_rk4_dense(None, None, None, 8, 4, -1e-3, 10, None, None) == _native.OSC_INVALID
+    assert lib.osc_equation_engine(None, None, None, None, 65, 1e-3, 10, 1, None, None, None,
+                                   None, None) == _native.OSC_INVALID
 
 
 def test_no_cpu_fallback():

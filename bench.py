@@ -38,10 +38,32 @@ METRIC = "DOF-steps/s"
 UNIT = "DOF-steps/s"
 HBM_BYTES_PER_DOF_STEP = 48  # read x,v,m,C + write x,v, one step per round trip
 FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42, "C5": 4 * 2 * 4096}
-# DP-pipe instructions per DOF-step in the hot loops, counted in SASS with
-# scripts/sass_stats.py --loop: batch2 176 per 2 systems per step
-# (NS=2); chain 380 per 8 cells (K=8, the default shape of both chain modes).
-DP_INST_PER_DOF_STEP = {"C1": 44, "C2": 44, "C3": 47.5, "C4": 47.5, "C5": None}
+# DP-pipe instructions per DOF-step in the hot loops: counted at run time in
+# the library's SASS (scripts/sass_stats.py; hot-loop kernel, DOFs advanced
+# per loop iteration), these constants only if cuobjdump is unavailable.
+DP_INST_PER_DOF_STEP = {"C1": 42, "C2": 42, "C3": 47, "C4": 47, "C5": None}
+DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb0ELi32E", 2),
+                  "C2": ("batch2_rk4_kernelILi2ELb0ELb0ELi256E", 4),
+                  "C3": ("chain_tiles_persistentILi8ELi256ELb0E", 8),
+                  "C4": ("chain_rk4_kernelILi8ELb0ELb0E", 8)}
+
+
+def dp_inst_per_dof_step(config: str):
+    """(count, source) for the roofline_fp64 denominator."""
+    if config not in DP_LOOP_KERNEL:
+        return None, None
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import sass_stats
+
+        kern, dofs = DP_LOOP_KERNEL[config]
+        n = sass_stats.dp_per_iteration(os.path.join(ROOT, "paper_1702_02207_b200",
+                                                     "libosc_b200.so"), kern)
+        if n:
+            return n / dofs, f"SASS of {kern}...: {n} DP instr per loop iteration / {dofs} DOFs"
+    except Exception:  # noqa: BLE001 -- cuobjdump missing: fall back to the counted constant
+        pass
+    return DP_INST_PER_DOF_STEP[config], "constant (counted with scripts/sass_stats.py --loop)"
 
 
 def peaks():
@@ -658,7 +680,7 @@ def main():
                     f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
                     f"is expected; its real limit is the FP64 pipe (roofline_fp64)",
         }
-    dp = DP_INST_PER_DOF_STEP[wl.name]
+    dp, dp_src = dp_inst_per_dof_step(wl.name)
     dp_inst_rate = per_gpu * dp if dp else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -675,7 +697,7 @@ def main():
                                    "IEEE fp64, byte-identical to oscbench.integrate")),
         "roofline": roofline,
         "roofline_fp64": {
-            "bound": "fp64_pipe", "dp_inst_per_dof_step": dp,
+            "bound": "fp64_pipe", "dp_inst_per_dof_step": dp, "dp_count_source": dp_src,
             "achieved_dp_inst_per_s": dp_inst_rate, "peak_dp_inst_per_s": fp64,
             "frac": dp_inst_rate / fp64 if dp_inst_rate else None,
             "algorithmic_flops_per_dof_step": FLOPS_PER_DOF_STEP[wl.name],

@@ -37,7 +37,7 @@ __device__ __forceinline__ void accel2(double p0, double p1, double C0, double C
     const double f1 = mul(C1, d1);
     const double num0 = (A == Arith::Fma) ? __fma_rn(-C0, p0, f1) : add(mul(-C0, p0), f1);
     a0 = qdiv<A>(num0, m0, ok);
-    a1 = qdiv<A>(-f1, m1, ok);
+    a1 = qdiv_neg<A>(f1, m1, ok);
 }
 
 // One classical RK4 step (oscillator.py:208-231).  The combination sums are

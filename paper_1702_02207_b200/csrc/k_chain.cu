@@ -86,14 +86,17 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         double num;
+        // The free end's numerator -f is formed as (-0.0) - f: bit for bit
+        // -f (also for f = +-0), selected as an operand so no separate
+        // negation is issued.
         if constexpr (kPad) {
             const double fnext = (j + 1 < K) ? f[j + 1] : fr;
-            num = (j == t.lastj) ? -f[j] : sub(fnext, f[j]);
+            num = sub((j == t.lastj) ? -0.0 : fnext, f[j]);
             num = (j < t.validn) ? num : 1.0;
         } else if (j + 1 < K) {
             num = sub(f[j + 1], f[j]);
         } else {
-            num = t.last ? -f[j] : sub(fr, f[j]);
+            num = sub(t.last ? -0.0 : fr, f[j]);
         }
         a[j] = qdiv<A>(num, t.md[j], ok);
     }

@@ -12,8 +12,9 @@ from collections import Counter
 LIB = "paper_1702_02207_b200/libosc_b200.so"
 
 
-def functions():
-    out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+def functions(lib=LIB):
+    out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True,
+                         check=True).stdout
     cur, body = None, []
     for line in out.splitlines():
         m = re.match(r"\s+Function : (\S+)", line)
@@ -48,6 +49,15 @@ def loop_body(body):
                 if best is None or dp > best[0]:
                     best = (dp, seg)
     return best[1] if best else [i for _, i in body]
+
+
+def dp_per_iteration(lib, kernel_substr):
+    """DP-pipe instructions in the hot loop of the first kernel whose mangled
+    name contains kernel_substr (one loop iteration = one RK4 step)."""
+    for name, body in functions(lib):
+        if kernel_substr in name:
+            return sum(opcode(i) in ("DADD", "DMUL", "DFMA") for i in loop_body(body))
+    return None
 
 
 def main():

@@ -15,7 +15,11 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-        "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers"]
+        "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "sm__sass_thread_inst_executed_op_dfma_pred_on.sum",
+        "sm__sass_thread_inst_executed_op_dmul_pred_on.sum",
+        "sm__sass_thread_inst_executed_op_dadd_pred_on.sum"]
 # report -> (kernel key used by bench.py, config)
 REPORTS = {"prof_batch2": ("batch2_rk4_kernel", "C2"),
            "prof_c3": ("chain_tiles_persistent<8,256>", "C3"),

@@ -586,10 +586,14 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     const size_t bytes = cells * sizeof(double);
     const size_t nsamp = xs ? static_cast<size_t>(1 + nsteps / stride) : 0;
 
-    // chunking: >= 8 MB of state per chunk, at most 8 chunks
+    // Chunking, so that only the first chunk's H2D and the last one's D2H are
+    // exposed: >= 2 MB of state per chunk, at most 8 chunks; 2-DOF chunks
+    // keep >= 148*1024 systems so each launch keeps K1's throughput shape.
     int64_t nchunk = 1;
     if (!xs && B > 1)
-        nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 23)}));
+        nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 21)}));
+    if (!chains)
+        nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 1024)));
     const int nstream = static_cast<int>(std::min<int64_t>(nchunk, 3));
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
     for (int i = 0; i < nstream; ++i)
@@ -611,7 +615,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         }
     } cleanup{streams, nstream};
 
-    const size_t total = 4 * bytes + B * sizeof(int64_t) + 2 * nsamp * bytes;
+    const size_t total = 4 * bytes + B * sizeof(int64_t) + 2 * nsamp * bytes + 16;
     OSC_CUDA(cudaMallocAsync(&cleanup.mem, total, streams[0]));
     cudaEvent_t ready;
     OSC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -625,6 +629,8 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     int64_t *dfb = reinterpret_cast<int64_t *>(dv + cells);
     double *dxs = xs ? reinterpret_cast<double *>(dfb + B) : nullptr;
     double *dvs = xs ? dxs + nsamp * cells : nullptr;
+    unsigned long long *dworst = reinterpret_cast<unsigned long long *>(
+        reinterpret_cast<double *>(dfb + B) + 2 * nsamp * cells);
     const auto H2D = cudaMemcpyHostToDevice;
     const auto D2H = cudaMemcpyDeviceToHost;
 
@@ -668,15 +674,22 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         OSC_CUDA(cudaMemcpyAsync(xs, dxs, nsamp * bytes, D2H, streams[0]));
         OSC_CUDA(cudaMemcpyAsync(vs, dvs, nsamp * bytes, D2H, streams[0]));
     }
+    // earliest divergence, reduced on the device once every chunk is done
+    for (int i = 1; i < nstream; ++i) {
+        cudaEvent_t done;
+        OSC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        OSC_CUDA(cudaEventRecord(done, streams[i]));
+        OSC_CUDA(cudaStreamWaitEvent(streams[0], done, 0));
+        cudaEventDestroy(done);
+    }
+    OSC_CUDA(osc::launch_first_bad(dfb, B, dworst, streams[0]));
+    unsigned long long worst[2];
+    OSC_CUDA(cudaMemcpyAsync(worst, dworst, sizeof worst, D2H, streams[0]));
     for (int i = 0; i < nstream; ++i)
         OSC_CUDA(cudaStreamSynchronize(streams[i]));
-    int64_t worst = -1;
-    for (int64_t b = 0; b < B; ++b)
-        if (first_bad[b] != 0 && (worst < 0 || first_bad[b] < first_bad[worst]))
-            worst = b;
-    if (worst >= 0)
+    if (worst[0] != ~0ull)
         return fail(OSC_NONFINITE, "integration diverged at step %lld (system %lld)",
-                    (long long)first_bad[worst], (long long)worst);
+                    (long long)worst[0], (long long)worst[1]);
     return OSC_OK;
 }
 

@@ -5,6 +5,8 @@
 #include "osc_device.cuh"
 #include "osc_kernels.h"
 
+#include <algorithm>
+
 namespace osc {
 namespace {
 
@@ -165,7 +167,52 @@ __global__ void dmma_peak_kernel(int64_t iters, int mode, double *sink)
         sink[threadIdx.x] = s;
 }
 
+// Earliest divergence over a batch: out[0] = min positive first_bad (or
+// ~0 if none), out[1] = the smallest index holding it.  Two atomic passes;
+// out must be preset to {~0, ~0}.
+__global__ void first_bad_step_kernel(const int64_t *__restrict__ fb, int64_t B,
+                                      unsigned long long *out)
+{
+    unsigned long long best = ~0ull;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (fb[i] > 0)
+            best = min(best, static_cast<unsigned long long>(fb[i]));
+    for (int o = 16; o > 0; o >>= 1)
+        best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0 && best != ~0ull)
+        atomicMin(&out[0], best);
+}
+
+__global__ void first_bad_index_kernel(const int64_t *__restrict__ fb, int64_t B,
+                                       unsigned long long *out)
+{
+    const unsigned long long step = out[0];
+    if (step == ~0ull)
+        return;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (static_cast<unsigned long long>(fb[i]) == step)
+            atomicMin(&out[1], static_cast<unsigned long long>(i));
+}
+
 }  // namespace
+
+cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *out,
+                             cudaStream_t stream)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 4, (B + 255) / 256)));
+    cudaError_t e = cudaMemsetAsync(out, 0xff, 2 * sizeof(unsigned long long), stream);
+    if (e != cudaSuccess)
+        return e;
+    first_bad_step_kernel<<<grid, 256, 0, stream>>>(fb, B, out);
+    first_bad_index_kernel<<<grid, 256, 0, stream>>>(fb, B, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lanes_ops,
                              cudaStream_t stream)

@@ -63,6 +63,11 @@ cudaError_t launch_energy(const double *m, const double *C, const double *x, con
                           double *out, int64_t B, int64_t s, bool cell_major,
                           cudaStream_t stream);
 
+// Earliest divergence of a batch on the device: out[0] = min positive step,
+// out[1] = its smallest index (both ~0 when nothing diverged).
+cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *out,
+                             cudaStream_t stream);
+
 cudaError_t launch_check_division(int64_t n, uint64_t seed, int mode,
                                   unsigned long long *mismatches, cudaStream_t stream);
 

@@ -31,11 +31,17 @@ def _stream(stream=None) -> int:
 
 
 def _dev(a, device=None) -> torch.Tensor:
-    """Contiguous float64 CUDA tensor (no copy when already one)."""
+    """Contiguous float64 CUDA tensor (no copy when already one).  Work runs
+    on the current CUDA device (the stream is its current stream), so a
+    tensor on another GPU is refused rather than launched against."""
     if isinstance(a, torch.Tensor):
         t = a
         if not t.is_cuda:
             t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
+        elif t.device.index != torch.cuda.current_device():
+            raise ValueError(f"tensor on {t.device} but the current device is "
+                             f"cuda:{torch.cuda.current_device()}; call inside "
+                             f"torch.cuda.device({t.device})")
     else:
         t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
             device or torch.device("cuda", torch.cuda.current_device()))

@@ -42,7 +42,7 @@ FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42, "C5": 4 * 2 * 4096
 # the library's SASS (scripts/sass_stats.py; hot-loop kernel, DOFs advanced
 # per loop iteration), these constants only if cuobjdump is unavailable.
 DP_INST_PER_DOF_STEP = {"C1": 42, "C2": 42, "C3": 47, "C4": 47, "C5": None}
-DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb0ELi32E", 2),
+DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb1ELi256E", 2),
                   "C2": ("batch2_rk4_kernelILi2ELb0ELb0ELi256E", 4),
                   "C3": ("chain_tiles_persistentILi8ELi256ELb0E", 8),
                   "C4": ("chain_rk4_kernelILi8ELb0ELb0E", 8)}

@@ -112,7 +112,8 @@ constexpr int kChunk = 64;  // steps between divergence checks
 // system j of thread t in block b is b*NS*blockDim + j*blockDim + t, so each
 // load/store of a warp stays one contiguous 256 B run.  Indices past B
 // duplicate the last system and are never stored.  kCmp: also accumulate
-// compare() against the analytic solution at every retained sample.
+// compare() against the analytic solution at every retained sample (when
+// cmp.sol is set).
 template <int NS, bool kFma, bool kCmp = false, int kMaxThreads = 256>
 __global__ void __launch_bounds__(kMaxThreads)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
@@ -151,9 +152,11 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
     }
     ErrAcc acc[kCmp ? NS : 1];
     if constexpr (kCmp) {
+        if (cmp.sol) {
 #pragma unroll
-        for (int j = 0; j < NS; ++j)
-            acc[j].add_sample(load_modal(cmp.sol, B, idx[j]), cmp.ts[0], s[j].x0, s[j].x1);
+            for (int j = 0; j < NS; ++j)
+                acc[j].add_sample(load_modal(cmp.sol, B, idx[j]), cmp.ts[0], s[j].x0, s[j].x1);
+        }
     }
     int64_t bad[NS];
 #pragma unroll
@@ -223,7 +226,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             }
         }
         if constexpr (kCmp) {
-            if (kstep % stride == 0) {
+            if (cmp.sol && kstep % stride == 0) {
 #pragma unroll
                 for (int j = 0; j < NS; ++j)
                     if (bad[j] == 0)
@@ -249,9 +252,11 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             first_bad[i] = bad[j];
             if constexpr (kCmp) {
                 const double nan = __longlong_as_double(0x7ff8000000000000ll);
+                if (cmp.sol) {
                 cmp.out[i] = bad[j] ? nan : acc[j].max_err;
                 cmp.out[B + i] = bad[j] ? nan : acc[j].rmse();
                 cmp.out[2 * B + i] = bad[j] ? nan : acc[j].at_time;
+                }
             }
         }
     }
@@ -266,11 +271,12 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
     const int64_t per_block = int64_t(threads) * NS;
     const unsigned blocks = static_cast<unsigned>((B + per_block - 1) / per_block);
     if (NS == 1 && !cmp && !fma && threads == 32) {
-        // Latency path (few systems, e.g. C1): the 32-thread bound gives ptxas
-        // a register budget whose schedule of the serial step is ~12% shorter
-        // (profiles/r01/c1_latency.md).
-        batch2_rk4_kernel<1, false, false, 32><<<blocks, threads, 0, stream>>>(
-            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
+        // Latency path (few systems, e.g. C1).  The time loop is the same
+        // 113 instructions in every build, but ptxas schedules the serial step
+        // of the compare build (its compare switched off: null CmpArgs) ~4%
+        // shorter than the others (profiles/r01/c1_latency.md).
+        batch2_rk4_kernel<1, false, true><<<blocks, threads, 0, stream>>>(
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, CmpArgs{});
         return cudaGetLastError();
     }
     if (cmp) {

@@ -1,9 +1,7 @@
-# C1 latency vs the K1 latency-path build, plus the C2 headline for the same build.
+# C1 latency: default latency build vs the compare build with compare off.
 mkdir -p gpurun_out
-for lb in 0 32; do
-  OSC_B2_LB=$lb OSC_B2=1,32 timeout 300 python bench.py --config C1 --no-cpu --no-e2e --steps 5 \
-    > gpurun_out/c1lat_$lb.json 2> gpurun_out/c1lat_$lb.err
-  python -c "import json; d=json.load(open('gpurun_out/c1lat_$lb.json')); print('C1 LB=$lb', d['ms_per_step'], 'ms/1e6 steps; validation', d['validation']['ms_per_step'])"
+for v in 0 1; do
+  if [ $v = 1 ]; then export OSC_B2_LATCMP=1; fi
+  timeout 300 python bench.py --config C1 --no-cpu --no-e2e --steps 5 > gpurun_out/c1v_$v.json 2> gpurun_out/c1v_$v.err
+  python -c "import json; d=json.load(open('gpurun_out/c1v_$v.json')); print('variant $v', d['ms_per_step'], 'validation', d['validation']['ms_per_step'])"
 done
-timeout 300 python bench.py --config C2 --no-cpu --no-e2e --steps 5 > gpurun_out/c2pin.json 2> gpurun_out/c2pin.err
-python -c "import json; d=json.load(open('gpurun_out/c2pin.json')); print('C2', d['ms_per_step'], d['roofline_fp64']['frac'], 'fma', d['fma_mode']['ms_per_step'], 'validation', d['validation']['ms_per_step'])"

@@ -511,6 +511,21 @@ def run_reference(args):
     return 0
 
 
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` started without torchrun: run it as N ranks, one per
+    GPU, exactly as the driver launches it."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -528,6 +543,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -548,8 +565,8 @@ def main():
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(backend)
-    if world > 1 and args.config == "C1":
-        raise SystemExit("C1 is one serial 2-DOF system: replicas only (DESIGN.md)")
+    # C1 is one serial 2-DOF system: at N > 1 every rank runs a replica
+    # (DESIGN.md "replicas only"); no collective on the data path.
 
     wl = Workload(args.config, rank, device, args.halo, world, args.transport)
     fp64 = fp64_peak(local)
@@ -689,7 +706,9 @@ def main():
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy PCG64, workloads.py; no dataset exists)",
         "config": dict(wl.desc, dt=wl.dt, nsteps_per_step=wl.nsteps,
-                       dof_steps_per_gpu_step=wl.dof_steps, parallelism=f"dp{world}",
+                       dof_steps_per_gpu_step=wl.dof_steps,
+                       parallelism={"C1": f"replicas{world}",
+                                    "C3": f"shards{world}"}.get(wl.name, f"dp{world}"),
                        l2="flushed between timed steps (256 MiB memset outside step events); "
                           "state is register-resident within a step",
                        arithmetic=("IEEE fp64; GEMM summation order differs from CPU BLAS "

@@ -61,9 +61,9 @@ osc::StepConsts consts(double dt)
 
 constexpr int64_t kWholeChainMax = 2048;  // 256 threads x 8 cells
 constexpr int64_t kWholeChainSteps = 512; // steps per launch in whole-chain mode
-// Tiled shape, measured on B200 for s = 2^24 (profiles/r01): with the
-// persistent prefetching kernel, 8 cells x 256 threads and 32-step halos
-// (2.57e11 DOF-steps/s) beat 8x128 (T=16: 2.36e11, T=32: 2.44e11).
+// Tiled shape, measured on B200 for s = 2^24 (profiles/r01/README.md): with
+// the persistent prefetching kernel, 8 cells x 256 threads and 32-step halos
+// beat 8 x 128 at T = 16..24 by 3-8% and 4 x 256 / 4 x 512 by 12-14%.
 constexpr int kTileK = 8, kTileThreads = 256;
 constexpr int64_t kTile = int64_t(kTileK) * kTileThreads;
 constexpr int64_t kDefaultHaloSteps = 32;
@@ -71,8 +71,8 @@ constexpr int64_t kDefaultHaloSteps = 32;
 void pick_whole(int64_t s, int &K, int &threads)
 {
     // Fewest cells per thread that keep the CTA at <= 128 threads, else 256
-    // threads of 8 cells.  Measured on B200 for s = 1024 (profiles/r01):
-    // K=8 x 128 threads 2.81e11 DOF-steps/s, K=4 x 256 2.61e11, K=2 x 512 1.19e11.
+    // threads of 8 cells.  Measured on B200 for s = 1024 (profiles/r01
+    // sweep_C4_*): K=8 x 128 threads beats K=4 x 256 by 8% and K=2 x 512 by 2.4x.
     K = 8;
     for (int k : {1, 2, 4, 8}) {
         if ((s + k - 1) / k <= 128) {

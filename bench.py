@@ -57,8 +57,9 @@ def dp_inst_per_dof_step(config: str):
         import sass_stats
 
         kern, dofs = DP_LOOP_KERNEL[config]
-        n = sass_stats.dp_per_iteration(os.path.join(ROOT, "paper_1702_02207_b200",
-                                                     "libosc_b200.so"), kern)
+        from paper_1702_02207_b200 import _native
+
+        n = sass_stats.dp_per_iteration(_native.LIB_PATH, kern)
         if n:
             return n / dofs, f"SASS of {kern}...: {n} DP instr per loop iteration / {dofs} DOFs"
     except Exception:  # noqa: BLE001 -- cuobjdump missing: fall back to the counted constant

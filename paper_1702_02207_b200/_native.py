@@ -11,7 +11,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libosc_b200.so")
+# OSC_LIB: load another build of the same library (compiler-option sweeps in
+# scripts/; the product default is the in-tree build).
+LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
 ABI_VERSION = 5

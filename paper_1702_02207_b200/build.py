@@ -41,16 +41,19 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = OUT,
+          build_dir: str = BUILD) -> str:
+    """Compile every csrc/*.cu and link ``out``.  ``extra``: additional nvcc
+    flags (used by scripts/build_variants.py for compiler-option sweeps)."""
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(HERE, "..", "include", "osc_b200.h"))
     objs, jobs = [], []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + headers):
-            jobs.append([nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj])
+            jobs.append([nvcc(), *NVCC_FLAGS, *extra, "-c", src, "-o", obj])
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         for cmd, res in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True,
                                                                    text=True), jobs)):
@@ -59,12 +62,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(res.stdout + res.stderr)
             if res.returncode:
                 raise RuntimeError(f"nvcc failed on {cmd[-3]}")
-    if force or jobs or _newer(OUT, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+    if force or jobs or _newer(out, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", out, *objs, "-lcudart"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode:
             raise RuntimeError("link failed:\n" + res.stdout + res.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

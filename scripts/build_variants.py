@@ -1,0 +1,24 @@
+"""Build compiler-option variants of libosc_b200.so for a sweep on the GPU box:
+paper_1702_02207_b200/_variants/<tag>/libosc_b200.so, selected at run time with
+OSC_LIB=<path> (see scripts/gpu_sweep_ptxas.sh).  Same sources, same
+--fmad=false: every variant is held to the same byte-exact tests."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1702_02207_b200 import build  # noqa: E402
+
+VARIANTS = {
+    "rul2": ["-Xptxas", "--register-usage-level=2"],
+    "rul8": ["-Xptxas", "--register-usage-level=8"],
+    "rul10": ["-Xptxas", "--register-usage-level=10"],
+    "O2": ["-Xptxas", "-O2"],
+}
+
+if __name__ == "__main__":
+    base = os.path.join(build.HERE, "_variants")
+    for tag, flags in VARIANTS.items():
+        d = os.path.join(base, tag)
+        out = build.build(force=True, extra=flags, out=os.path.join(d, "libosc_b200.so"),
+                          build_dir=os.path.join(d, "obj"))
+        print(tag, out)

@@ -82,3 +82,24 @@ def test_local_group_peer_transport_divergence():
     fb = grp.run(300)
     ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 300, check=False)
     assert fb > 0 and fb == int(ref.first_bad[0])
+
+
+# property-based: random chain lengths, shard counts, steps per period and
+# transports all give the single-GPU bytes (parallel.py:11-14's contract)
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=100, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(s=st.integers(2_000, 60_000), shards=st.integers(1, 8), T=st.integers(1, 40),
+       nsteps=st.integers(1, 150), transport=st.sampled_from(["nccl", "peer"]),
+       seed=st.integers(0, 2**32 - 1))
+def test_local_group_random_decompositions(s, shards, T, nsteps, transport, seed):
+    if s // shards < 4 * T + 2:
+        shards = max(1, s // (4 * T + 2))  # each shard must hold its 2T-cell ghost zones
+    m, C, x0, v0 = _chain(s, seed)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, shards, halo_steps=T, transport=transport)
+    assert grp.run(nsteps) == 0
+    x, v = grp.gather()
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, nsteps)
+    assert bits(x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
+    assert bits(v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())

@@ -102,6 +102,16 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
     }
 }
 
+// A buffer whose divergence was recorded in an EARLIER launch (first_bad <=
+// step0) is skipped: integrate has raised, its state is unspecified.  A step
+// recorded during this launch by another tile must not skip this one, which
+// may hold an earlier step of the same launch (tiles run in any order).
+__device__ __forceinline__ bool diverged_before(const SegArgs &g, int64_t buf)
+{
+    const int64_t fb = g.first_bad[buf];
+    return fb != 0 && fb <= g.step0;
+}
+
 // Zero every slot (sentinels included); callers then __syncthreads().
 __device__ __forceinline__ void edges_init(Edges &e)
 {
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
     // and the exit must be uniform across this CTA's barriers.
     edges_init(edges);
     if (threadIdx.x == 0)
-        s_skip = g.first_bad[buf_id] != 0;
+        s_skip = diverged_before(g, buf_id);
     __syncthreads();
     if (s_skip)
         return;  // already diverged: state is unspecified, as integrate raised
@@ -391,7 +401,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
         const TileGeom tg = tile_geom(g, it, TILE);
         const int64_t c0 = tg.L + cl;
         if (threadIdx.x == 0)  // uniform skip decision (see chain_rk4_kernel)
-            s_skip = g.first_bad[tg.buf_id] != 0;
+            s_skip = diverged_before(g, tg.buf_id);
         __syncthreads();
         if (!s_skip) {
             bool ok = true;

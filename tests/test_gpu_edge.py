@@ -139,3 +139,25 @@ def test_batch_parameter_validation_mirrors_reference():
     m = ok.copy()
     m[0, 0] = 5e-324
     batched.integrate_batch2(m, ok, ok * 0, ok * 0, 1e-3, 5)
+
+
+def test_divergence_step_not_lost_to_tile_order():
+    """Regression: a tile must not skip because ANOTHER tile of the same
+    launch already recorded a (later) divergence step.  Persistent tiled
+    kernel, 148 CTAs striding over 170 tiles: tiles 10 and 20 diverge in
+    round one (steps ~35, ~36; their exact replays delay their CTAs), tile
+    168 -- CTA 20's second tile -- holds the earliest step (~34)."""
+    W = 2048 - 4 * 32  # owned cells per tile at the default 32 steps per launch
+    s = 170 * W
+    rng = np.random.default_rng(21)
+    m = rng.uniform(0.5, 2.0, s)
+    C = rng.uniform(500.0, 2000.0, s)
+    x0 = rng.standard_normal(s)
+    v0 = np.zeros(s)
+    for tile, c in ((10, 6.0e10), (20, 4.0e10), (168, 9.0e10)):
+        C[tile * W + W // 2] = c
+    res = batched.integrate_chains(m, C, x0, v0, 1e-3, 64, check=False)
+    _, _, _, _, fb = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 64,
+                                         sample=False)
+    assert 32 < fb[0] <= 64
+    assert int(res.first_bad[0]) == int(fb[0])

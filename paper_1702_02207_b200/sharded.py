@@ -330,15 +330,22 @@ class ShardedChain:
         k = 0
         while k < nsteps:
             n = min(self.T, nsteps - k)
-            self.phase_interior(n, k)
-            if self.world > 1:
-                if self.cuda:
-                    main = torch.cuda.current_stream(self.device)
-                    self.comm_stream.wait_stream(main)
-                    with torch.cuda.stream(self.comm_stream):
-                        self._exchange(self.x, self.v)
-                    main.wait_stream(self.comm_stream)
-                else:
+            if self.world > 1 and self.cuda:
+                # The exchange needs only the previous period's output, not the
+                # interior tiles: it waits on an event recorded BEFORE they are
+                # enqueued, so it overlaps them (interior tiles read owned cells
+                # only; the exchange reads boundary cells and writes ghosts).
+                main = torch.cuda.current_stream(self.device)
+                ready = torch.cuda.Event()
+                ready.record(main)
+                self.phase_interior(n, k)
+                self.comm_stream.wait_event(ready)
+                with torch.cuda.stream(self.comm_stream):
+                    self._exchange(self.x, self.v)
+                main.wait_stream(self.comm_stream)
+            else:
+                self.phase_interior(n, k)
+                if self.world > 1:
                     self._exchange(self.x, self.v)
             self.phase_edges(n, k)
             k += n

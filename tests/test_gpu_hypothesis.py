@@ -73,3 +73,71 @@ def test_chains_random(B, s, nsteps, sdiv, halo, dt, seed, special):
     gx, gv = res.xs.cpu().numpy(), res.vs.cpu().numpy()
     assert bits(gx[:, ok]) == bits(xs[:, ok]) and bits(gv[:, ok]) == bits(vs[:, ok])
     assert bits(res.x.cpu().numpy()[ok]) == bits(xo[ok])
+
+
+@settings(max_examples=30, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(B=st.integers(1, 700_000), nsteps=st.integers(1, 60), seed=st.integers(0, 2**32 - 1))
+def test_batch2_host_path_random(B, nsteps, seed):
+    """Host-pointer C ABI (chunked, multi-stream) == device path, bit for bit."""
+    from paper_1702_02207_b200 import _native
+
+    rng = np.random.default_rng(seed)
+    m, C, x0, v0 = _draw_state(rng, (2, B), seed % 2 == 0)
+    x, v = x0.copy(), v0.copy()
+    fb = np.zeros(B, dtype=np.int64)
+    rc = _native.lib().osc_rk4_batch2_host(m.ctypes.data, C.ctypes.data, x.ctypes.data,
+                                           v.ctypes.data, B, 1e-3, nsteps, nsteps, None, None,
+                                           fb.ctypes.data)
+    res = batched.integrate_batch2(m, C, x0, v0, 1e-3, nsteps, check=False)
+    dfb = res.first_bad.cpu().numpy()
+    assert fb.tolist() == dfb.tolist()
+    assert rc == (_native.OSC_NONFINITE if dfb.any() else _native.OSC_OK)
+    ok = dfb == 0
+    assert bits(x[:, ok]) == bits(res.x.cpu().numpy()[:, ok])
+    assert bits(v[:, ok]) == bits(res.v.cpu().numpy()[:, ok])
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(B=st.integers(1, 500), nsteps=st.integers(1, 80), sdiv=st.integers(1, 5),
+       seed=st.integers(0, 2**32 - 1), chains=st.booleans(), s=st.integers(1, 3000))
+def test_sample_energies_random(B, nsteps, sdiv, seed, chains, s):
+    """energy() of every retained sample, computed on the device, equals the
+    (reference-pinned) oracle's energy of the same sample bit for bit."""
+    rng = np.random.default_rng(seed)
+    stride = max(1, nsteps // sdiv)
+    if chains:
+        B = min(B, 4)
+        m, C, x0, v0 = _draw_state(rng, (B, s), False)
+        res = batched.integrate_chains(m, C, x0, v0, 1e-4, nsteps, stride, sample=True,
+                                       energies=True, check=False)
+        xs, vs = res.xs.cpu().numpy(), res.vs.cpu().numpy()  # [nsamp][B][s]
+        es = res.energies.cpu().numpy()
+        for k in range(xs.shape[0]):
+            assert bits(es[k]) == bits(oracle.c_energy(m, C, xs[k], vs[k]))
+    else:
+        m, C, x0, v0 = _draw_state(rng, (2, B), False)
+        res = batched.integrate_batch2(m, C, x0, v0, 1e-4, nsteps, stride, sample=True,
+                                       energies=True, check=False)
+        xs, vs = res.xs.cpu().numpy(), res.vs.cpu().numpy()  # [nsamp][2][B]
+        es = res.energies.cpu().numpy()
+        for k in range(xs.shape[0]):
+            assert bits(es[k]) == bits(oracle.c_energy(m.T, C.T, xs[k].T, vs[k].T))
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(s=st.integers(1, 300), N=st.integers(1, 90), nsteps=st.integers(1, 25),
+       seed=st.integers(0, 2**32 - 1))
+def test_dense_random_shapes(s, N, nsteps, seed):
+    """Padded dense path (s -> x128, N -> x32) vs the numpy restatement,
+    relative 1e-10 (GEMM summation order)."""
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(0.5, 2.0, s)
+    q, _ = np.linalg.qr(rng.standard_normal((s, s)))
+    K = (q * rng.uniform(500.0, 2000.0, s)) @ q.T
+    K = 0.5 * (K + K.T)
+    A = K / m[:, None]
+    X0, V0 = rng.standard_normal((s, N)), rng.standard_normal((s, N))
+    res = batched.integrate_dense(A, X0, V0, 1e-4, nsteps)
+    Xo, Vo = oracle.dense_rk4(A, X0, V0, 1e-4, nsteps)
+    for got, ref in ((res.x.cpu().numpy(), Xo), (res.v.cpu().numpy(), Vo)):
+        assert np.max(np.abs(got - ref)) <= 1e-10 * max(1.0, np.max(np.abs(ref)))

@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 5
+#define OSC_ABI_VERSION 6
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -132,6 +132,20 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
                           int64_t step0, int64_t *first_bad, const osc_peer_t *left,
                           const osc_peer_t *right, uint32_t flags, void *stream);
+
+/* One chain of s cells sharded over the GPUs of THIS process (devs[ngpu],
+ * ids may repeat), host buffers m, C, x, v [s] (x, v updated in place),
+ * byte-identical to osc_rk4_chains for any ngpu.  Contiguous shards with
+ * 2*halo_steps ghost cells per interior side (0 = default 32); every
+ * halo_steps steps each shard's tile kernel stores its boundary cells
+ * straight into its neighbours' next-input ghost zones (peer memory over
+ * NVLink, peer access enabled here) -- the fused exchange of
+ * osc_rk4_chain_advance, ordered by cross-device events only.  The
+ * single-process counterpart of the one-process-per-GPU driver
+ * (paper_1702_02207_b200/sharded.py).  Synchronous.  first_bad: [1]. */
+int osc_rk4_chain_sharded(int ngpu, const int *devs, const double *m, const double *C, double *x,
+                          double *v, int64_t s, double dt, int64_t nsteps, int64_t halo_steps,
+                          int64_t *first_bad, uint32_t flags);
 
 /* Dense general system M x'' + K x = 0 (BASELINE configs[4]; outside the
  * reference).  osc_rowscale: A = K / m[:, None] (IEEE division

@@ -264,6 +264,30 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
     return res.check() if check else res
 
 
+def integrate_chain_sharded(m, C, x0, v0, dt, nsteps, devices, *, halo_steps=0, fma=False):
+    """One chain over several GPUs of this process (osc_rk4_chain_sharded):
+    host arrays in, final host ``(x, v)`` out, byte-identical to
+    ``integrate_chains`` for any device list (ids may repeat).  Raises
+    NonFiniteStateError(step) like integrate."""
+    lib = _native.lib()
+    m, C = (np.ascontiguousarray(a, np.float64) for a in (m, C))
+    x, v = (np.array(a, np.float64, order="C") for a in (x0, v0))
+    if not (m.shape == C.shape == x.shape == v.shape) or m.ndim != 1:
+        raise ValueError("expected four [s] arrays")
+    validate_parameters(torch.from_numpy(m), torch.from_numpy(C))
+    devs = (ctypes.c_int * len(devices))(*devices)
+    fb = np.zeros(1, np.int64)
+    rc = lib.osc_rk4_chain_sharded(len(devices), devs, m.ctypes.data, C.ctypes.data,
+                                   x.ctypes.data, v.ctypes.data, m.size, float(dt), int(nsteps),
+                                   int(halo_steps), fb.ctypes.data,
+                                   _native.OSC_FMA if fma else 0)
+    if rc == _native.OSC_NONFINITE:
+        raise NonFiniteStateError(f"integration diverged at step {int(fb[0])}",
+                                  step=int(fb[0]))
+    raise_for(rc, "osc_rk4_chain_sharded")
+    return x, v
+
+
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
                   stream=None, fma=False, left=None, right=None):
     """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance).

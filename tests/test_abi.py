@@ -77,6 +77,14 @@ def test_argument_errors_need_no_device(lib):
     assert lib.osc_rk4_batch2_compare(None, None, None, None, 4, 1e-3, 10, 1, None, None, None,
                                       None, 0, None) == _native.OSC_INVALID
     assert b"null buffer" in lib.osc_last_error()
+    # single-process sharded chains validate before touching any device
+    devs = (ctypes.c_int * 2)(0, 0)
+    assert lib.osc_rk4_chain_sharded(0, devs, None, None, None, None, 100, 1e-3, 10, 0, None,
+                                     0) == _native.OSC_INVALID
+    assert lib.osc_rk4_chain_sharded(2, devs, None, None, None, None, 100, -1.0, 10, 0, None,
+                                     0) == _native.OSC_INVALID
+    assert lib.osc_rk4_chain_sharded(2, devs, None, None, None, None, 100, 1e-3, 10, 100, None,
+                                     0) == _native.OSC_INVALID
     # dense and engine paths check shapes before touching the device
     assert lib.osc_rk4_dense(None, None, None, 0, 4, 1e-3, 10, None, None) == _native.OSC_INVALID
     assert lib.osc_rk4_dense(None, None, None, 8, 4, -1e-3, 10, None, None) == _native.OSC_INVALID

@@ -103,3 +103,42 @@ def test_local_group_random_decompositions(s, shards, T, nsteps, transport, seed
     ref = batched.integrate_chains(m, C, x0, v0, 1e-3, nsteps)
     assert bits(x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
     assert bits(v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())
+
+
+# --------------------------------------------------------------------------
+# single-process multi-GPU C entry (osc_rk4_chain_sharded); one device here,
+# so the shards share cuda:0 -- the kernels never wait on one another
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("shards,T", [(1, 32), (2, 32), (3, 16), (5, 7), (8, 32)])
+def test_c_entry_sharded_chain_bit_identical(shards, T):
+    s = 150_001
+    m, C, x0, v0 = _chain(s, shards + 100)
+    x, v = batched.integrate_chain_sharded(m, C, x0, v0, 1e-3, 131, [0] * shards, halo_steps=T)
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 131)
+    assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
+
+
+def test_c_entry_sharded_chain_divergence():
+    import paper_1702_02207_b200 as osc
+
+    s = 80_000
+    m, C, x0, v0 = _chain(s, 5)
+    C[61_000] = 1e8
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 300, check=False)
+    with pytest.raises(osc.NonFiniteStateError) as e:
+        batched.integrate_chain_sharded(m, C, x0, v0, 1e-3, 300, [0, 0, 0, 0])
+    assert e.value.step == int(ref.first_bad[0]) > 0
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(s=st.integers(2_000, 40_000), shards=st.integers(1, 6), T=st.integers(1, 40),
+       nsteps=st.integers(1, 120), seed=st.integers(0, 2**32 - 1))
+def test_c_entry_sharded_random(s, shards, T, nsteps, seed):
+    if s // shards < 2 * T:
+        shards = max(1, s // (2 * T))
+    m, C, x0, v0 = _chain(s, seed)
+    x, v = batched.integrate_chain_sharded(m, C, x0, v0, 1e-3, nsteps, [0] * shards,
+                                           halo_steps=T)
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, nsteps)
+    assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())

@@ -3,8 +3,10 @@
  * no Python, no torch.  Integrates a batch of independent 2-DOF systems
  * (BASELINE configs[1] shape, smaller B) twice -- through the synchronous
  * host-pointer entry point and through the device-pointer one on a CUDA
- * stream -- checks the two agree bit for bit, and shows the error contract
- * (OSC_INVALID for a bad dt, OSC_NONFINITE + first_bad for a divergent system).
+ * stream -- checks the two agree bit for bit, shows the error contract
+ * (OSC_INVALID for a bad dt, OSC_NONFINITE + first_bad for a divergent system)
+ * and runs one chain sharded over the GPUs of the process (osc_rk4_chain_sharded)
+ * against the single-GPU chain.
  *
  * build:  gcc -O2 -I include examples/c_abi_demo.c -o c_abi_demo \
  *           -L paper_1702_02207_b200 -l:libosc_b200.so -L/usr/local/cuda/lib64 -lcudart \
@@ -121,8 +123,32 @@ int main(int argc, char **argv)
         fprintf(stderr, "divergence not reported (rc=%d, step=%lld)\n", rc, (long long)bad);
         return 1;
     }
-    printf("ok: %d systems x %d steps, host == device form, diverging system tagged at step "
-           "%lld (%s)\n", B, NSTEPS, (long long)bad, osc_last_error());
+    /* 4. one chain sharded over the GPUs of this process (here: device 0
+     *    twice) == the single-GPU chain, byte for byte */
+    {
+        enum { S = 20000, STEPS = 100 };
+        static double cm[S], cc[S], cx[S], cv[S], cx2[S], cv2[S];
+        for (int i = 0; i < S; ++i) {
+            cm[i] = 0.5 + 1.5 * urand(&seed);
+            cc[i] = 500.0 + 1500.0 * urand(&seed);
+            cx[i] = cx2[i] = 2.0 * urand(&seed) - 1.0;
+            cv[i] = cv2[i] = 0.0;
+        }
+        int64_t fb1 = 0, fb2 = 0;
+        const int devs[2] = {0, 0};
+        if (osc_rk4_chains_host(cm, cc, cx, cv, 1, S, 1e-3, STEPS, STEPS, NULL, NULL, &fb1) != OSC_OK ||
+            osc_rk4_chain_sharded(2, devs, cm, cc, cx2, cv2, S, 1e-3, STEPS, 0, &fb2, 0) != OSC_OK) {
+            fprintf(stderr, "chain calls failed: %s\n", osc_last_error());
+            return 1;
+        }
+        if (memcmp(cx, cx2, sizeof cx) || memcmp(cv, cv2, sizeof cv)) {
+            fprintf(stderr, "sharded chain differs from the single-GPU chain\n");
+            return 1;
+        }
+    }
+    printf("ok: %d systems x %d steps, host == device form, sharded chain == single chain, "
+           "diverging system tagged at step %lld (%s)\n", B, NSTEPS, (long long)bad,
+           osc_last_error());
     cudaFree(dm);
     cudaFree(dC);
     cudaFree(dx);

@@ -188,7 +188,7 @@ def _energies(nsteps, stride, B, device, want):
 
 def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
                      compare=False, analytic=None, fma=False, validate=True, stream=None,
-                     check=True) -> BatchResult:
+                     check=True, t0=0.0) -> BatchResult:
     """Independent 2-DOF systems, SoA ``[2][B]`` (oscillator.py:194-263 for s = 2).
 
     ``validate`` applies OscillatorSystem's parameter rule to the batch (one
@@ -211,7 +211,7 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
     if compare:
         sol = _dev(analytic) if analytic is not None else analytic_batch2(m, C, x0, v0,
                                                                          stream=stream)
-        ts = _dev(accumulated_times(0.0, float(dt), int(nsteps), int(stride)))
+        ts = _dev(accumulated_times(float(t0), float(dt), int(nsteps), int(stride)))
     if compare and not (sample or energies):
         x, v = x0.clone(), v0.clone()
         xs = vs = es = None
@@ -233,15 +233,16 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
             bad = fb > 0
             for t in (errors.max_abs_error, errors.rmse, errors.at_time):
                 t.masked_fill_(bad, float("nan"))
-    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es,
-                      errors=errors)
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), float(t0),
+                      energies=es, errors=errors)
     return res.check() if check else res
 
 
 def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, energies=False,
                      halo_steps=0, fma=False, validate=True, stream=None,
-                     check=True) -> BatchResult:
-    """B wall-anchored chains of s cells, ``[B][s]`` (oscillator.py:152-263)."""
+                     check=True, t0=0.0) -> BatchResult:
+    """B wall-anchored chains of s cells, ``[B][s]`` (oscillator.py:152-263).
+    ``t0``: time label of the initial state (resume, as integrate_batch2)."""
     lib = _native.lib()
     stride = nsteps if stride is None else stride
     m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
@@ -260,7 +261,8 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
                             int(halo_steps), _native.OSC_FMA if fma else 0,
                             ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_chains")
-    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), energies=es)
+    res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), float(t0),
+                      energies=es)
     return res.check() if check else res
 
 

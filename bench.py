@@ -172,9 +172,10 @@ class Workload:
                          "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
         elif name == "C3":
             arrays = workloads.c3()
-            T = halo or 32
+            plan = batched.chain_plan(1, workloads.C3_S, p.nsteps, halo)
+            T = plan["steps_per_launch"]
             self.kernel = "chain_tiles_persistent<8,256>"
-            self.launches = -(-p.nsteps // T)
+            self.launches = plan["launches"]
             self.world = world
             self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",
                          "cells": workloads.C3_S, "halo_steps": T,

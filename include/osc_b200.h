@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 6
+#define OSC_ABI_VERSION 7
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -106,6 +106,12 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
                    int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
                    double *es, int64_t *first_bad, int64_t halo_steps, uint32_t flags,
                    void *stream);
+
+/* The launch plan osc_rk4_chains uses for B chains of s cells and nsteps
+ * steps (halo_steps as there; 0 = chosen here): plan[7] = {cells per thread,
+ * threads per CTA, steps per launch, owned cells per tile, halo cells per
+ * side, tiles per chain, launches without sampling}.  No device work. */
+int osc_chain_plan(int64_t B, int64_t s, int64_t nsteps, int64_t halo_steps, int64_t *plan);
 
 /* A neighbouring shard's next-input buffers for the fused halo exchange:
  * `count` boundary cells of ours (our first `count` owned cells for the left

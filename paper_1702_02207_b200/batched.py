@@ -290,6 +290,16 @@ def integrate_chain_sharded(m, C, x0, v0, dt, nsteps, devices, *, halo_steps=0, 
     return x, v
 
 
+def chain_plan(B, s, nsteps, halo_steps=0) -> dict:
+    """The launch plan integrate_chains uses (osc_chain_plan; no device work)."""
+    out = (ctypes.c_int64 * 7)()
+    raise_for(_native.load().osc_chain_plan(int(B), int(s), int(nsteps), int(halo_steps), out),
+              "osc_chain_plan")
+    keys = ("cells_per_thread", "threads", "steps_per_launch", "owned_per_tile", "halo",
+            "tiles_per_chain", "launches")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
                   stream=None, fma=False, left=None, right=None):
     """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance).

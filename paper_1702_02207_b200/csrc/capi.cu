@@ -86,6 +86,39 @@ void pick_whole(int64_t s, int &K, int &threads)
     threads = static_cast<int>(((t + 31) / 32) * 32);
 }
 
+// Steps per tiled launch when the caller leaves it to us.  A launch costs
+// rounds(T) tile-times of (T + c) steps, where rounds(T) = ceil(tiles(T) /
+// CTAs) (one persistent CTA per SM) and c ~ 4 steps covers a tile's load,
+// setup and store; per step that is rounds(T) * (T + c) / T.  Deeper halos
+// mean fewer launches but narrower owned tiles, so the tile count can cross
+// a multiple of the CTA count: for C3 (2^24 cells) T = 31 gives 59 rounds
+// instead of 60 (+0.7% measured, profiles/r01/README.md).
+int64_t pick_halo_steps(int64_t s, int64_t B, int64_t nsteps)
+{
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        sms = 148;            // no device (planning only): B200
+        cudaGetLastError();   // do not leave the query's error pending
+    }
+    constexpr double c = 4.0;
+    int64_t best = kDefaultHaloSteps;
+    double best_cost = 0.0;
+    for (int64_t T : {int64_t(32), int64_t(31), int64_t(30), int64_t(28)}) {
+        if (T > nsteps && T != kDefaultHaloSteps)
+            continue;
+        const int64_t W = kTile - 4 * T;
+        const int64_t tiles = B * ((s + W - 1) / W);
+        const int64_t rounds = (tiles + sms - 1) / sms;
+        const double cost = double(rounds) * (double(T) + c) / double(T);
+        if (best_cost == 0.0 || cost < best_cost * (1.0 - 1e-9)) {
+            best = T;
+            best_cost = cost;
+        }
+    }
+    return best;
+}
+
 // Tuning hook (benchmarks only): OSC_TILE="K,threads" / OSC_WHOLE="K,threads"
 // override the tiled / whole-chain launch shapes.  Read-only process state.
 bool env_shape(const char *name, int &K, int &threads)
@@ -99,6 +132,43 @@ bool env_shape(const char *name, int &K, int &threads)
     K = k;
     threads = t;
     return true;
+}
+
+struct ChainPlan {
+    int K = kTileK, threads = kTileThreads;
+    int64_t W = 0, H = 0, tiles = 1, per_launch = 0;
+};
+
+// Launch plan of osc_rk4_chains: whole chains up to kWholeChainMax cells
+// (one CTA per chain, kWholeChainSteps steps per launch), else temporally
+// blocked tiles of K x threads cells, H = 2T halo, T steps per launch.
+int plan_chain(int64_t s, int64_t B, int64_t nsteps, int64_t halo_steps, ChainPlan &p)
+{
+    int wk = 0, wt = 0;
+    const bool whole_env = env_shape("OSC_WHOLE", wk, wt) && int64_t(wk) * wt >= s;
+    if (s <= kWholeChainMax || whole_env) {
+        pick_whole(s, p.K, p.threads);
+        if (whole_env) {
+            p.K = wk;
+            p.threads = wt;
+        }
+        p.W = s;
+        p.H = 0;
+        p.tiles = 1;
+        p.per_launch = kWholeChainSteps;
+        return OSC_OK;
+    }
+    const bool shaped = env_shape("OSC_TILE", p.K, p.threads);
+    const int64_t T = halo_steps > 0 ? halo_steps
+                                     : (shaped ? kDefaultHaloSteps : pick_halo_steps(s, B, nsteps));
+    p.H = 2 * T;
+    p.W = int64_t(p.K) * p.threads - 2 * p.H;
+    if (p.W < 1)
+        return fail(OSC_INVALID, "halo_steps=%lld too deep for a %lld-cell tile", (long long)T,
+                    (long long)p.K * p.threads);
+    p.tiles = (s + p.W - 1) / p.W;
+    p.per_launch = T;
+    return OSC_OK;
 }
 
 // Keep freed stream-ordered allocations in the device's default pool instead
@@ -237,31 +307,14 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     g.own_hi = s;
     g.k = consts(dt);
     g.fma = (flags & OSC_FMA) != 0;
-    int K = kTileK, threads = kTileThreads;
-    int64_t per_launch;
-    int wk = 0, wt = 0;
-    const bool whole_env = env_shape("OSC_WHOLE", wk, wt) && int64_t(wk) * wt >= s;
-    if (s <= kWholeChainMax || whole_env) {
-        pick_whole(s, K, threads);
-        if (whole_env) {
-            K = wk;
-            threads = wt;
-        }
-        g.W = s;
-        g.H = 0;
-        g.tiles = 1;
-        per_launch = kWholeChainSteps;
-    } else {
-        const int64_t T = halo_steps > 0 ? halo_steps : kDefaultHaloSteps;
-        env_shape("OSC_TILE", K, threads);
-        g.H = 2 * T;
-        g.W = int64_t(K) * threads - 2 * g.H;
-        if (g.W < 1)
-            return fail(OSC_INVALID, "halo_steps=%lld too deep for a %lld-cell tile",
-                        (long long)T, (long long)K * threads);
-        g.tiles = (s + g.W - 1) / g.W;
-        per_launch = T;
-    }
+    ChainPlan plan;
+    if (int rc = plan_chain(s, B, nsteps, halo_steps, plan))
+        return rc;
+    const int K = plan.K, threads = plan.threads;
+    const int64_t per_launch = plan.per_launch;
+    g.W = plan.W;
+    g.H = plan.H;
+    g.tiles = plan.tiles;
 
     OSC_CUDA(cudaMemsetAsync(first_bad, 0, sizeof(int64_t) * B, stream));
     if (xs) {
@@ -311,6 +364,20 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
         OSC_CUDA(cudaMemcpyAsync(x, cx, bytes, cudaMemcpyDeviceToDevice, stream));
         OSC_CUDA(cudaMemcpyAsync(v, cv, bytes, cudaMemcpyDeviceToDevice, stream));
     }
+    return OSC_OK;
+}
+
+int osc_chain_plan(int64_t B, int64_t s, int64_t nsteps, int64_t halo_steps, int64_t *plan)
+{
+    if (B < 1 || s < 1 || nsteps < 1 || !plan)
+        return fail(OSC_INVALID, "need B, s, nsteps >= 1 and a plan buffer");
+    ChainPlan p;
+    if (int rc = plan_chain(s, B, nsteps, halo_steps, p))
+        return rc;
+    const int64_t launches = (nsteps + p.per_launch - 1) / p.per_launch;
+    const int64_t out[7] = {p.K, p.threads, p.per_launch, p.W, p.H, p.tiles, launches};
+    for (int i = 0; i < 7; ++i)
+        plan[i] = out[i];
     return OSC_OK;
 }
 

@@ -156,3 +156,19 @@ def test_workloads_are_seeded():
     assert not np.array_equal(r1[0], m)
     m, C, x0, v0 = workloads.c1()
     assert (C / m == 1012.5).all()
+
+
+def test_chain_launch_plan(lib):
+    """osc_chain_plan needs no device: the C3/C4 plans the bench reports."""
+    from paper_1702_02207_b200 import batched
+
+    c3 = batched.chain_plan(1, 1 << 24, 10_000)
+    # T = 31 fits 8720 tiles in 59 rounds of 148 CTAs (T = 32: 8739 tiles, 60)
+    assert c3["steps_per_launch"] == 31 and c3["launches"] == 323
+    assert c3["owned_per_tile"] == 2048 - 4 * 31 and c3["tiles_per_chain"] == 8720
+    assert batched.chain_plan(1, 1 << 24, 10_000, halo_steps=32)["tiles_per_chain"] == 8739
+    c4 = batched.chain_plan(4096, 1024, 10_000)
+    assert (c4["cells_per_thread"], c4["threads"], c4["steps_per_launch"], c4["launches"]) == \
+        (8, 128, 512, 20)
+    with pytest.raises(ValueError):
+        batched.chain_plan(1, 1 << 20, 100, halo_steps=600)

@@ -156,7 +156,7 @@ def test_divergence_step_not_lost_to_tile_order():
     v0 = np.zeros(s)
     for tile, c in ((10, 6.0e10), (20, 4.0e10), (168, 9.0e10)):
         C[tile * W + W // 2] = c
-    res = batched.integrate_chains(m, C, x0, v0, 1e-3, 64, check=False)
+    res = batched.integrate_chains(m, C, x0, v0, 1e-3, 64, check=False, halo_steps=32)
     _, _, _, _, fb = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 64,
                                          sample=False)
     assert 32 < fb[0] <= 64

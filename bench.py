@@ -106,10 +106,15 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # let nvidia-smi finish its driver initialisation (first sample)
+            # before the timed region, so that it cannot land inside a step
+            t_end = time.time() + 2.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
@@ -588,8 +593,8 @@ def main():
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    barrier()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local) as clocks:  # started (and settled) before the barrier
+        barrier()
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed steps, outside the step's events
             starts[i].record()

@@ -63,6 +63,7 @@ osc::StepConsts consts(double dt)
 
 constexpr int64_t kWholeChainMax = 2048;  // 256 threads x 8 cells
 constexpr int64_t kWholeChainSteps = 512; // steps per launch in whole-chain mode
+constexpr int64_t kSplitChains = 1024;     // whole-chain batches this large run as two halves
 // Tiled shape, measured on B200 for s = 2^24 (profiles/r01/README.md): with
 // the persistent prefetching kernel, 8 cells x 256 threads and 32-step halos
 // beat 8 x 128 at T = 16..24 by 3-8% and 4 x 256 / 4 x 512 by 12-14%.
@@ -330,41 +331,85 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     Scratch scratch;
     scratch.s = stream;
     OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch.p), 2 * bytes, stream));
-    double *cx = x, *cv = v, *nx = scratch.p, *nv = scratch.p + cells;
-    for (int64_t k0 = 0; k0 < nsteps;) {
-        int64_t n = nsteps - k0;
-        if (n > per_launch)
-            n = per_launch;
-        const int64_t next_sample = (k0 / stride + 1) * stride;
-        if (next_sample - k0 < n)
-            n = next_sample - k0;
-        g.xin = cx;
-        g.vin = cv;
-        g.xout = nx;
-        g.vout = nv;
-        g.nsteps = n;
-        g.step0 = k0;
-        const bool sample = xs && (k0 + n) % stride == 0;
-        g.xs = sample ? xs + ((k0 + n) / stride) * cells : nullptr;
-        g.vs = sample ? vs + ((k0 + n) / stride) * cells : nullptr;
-        cudaError_t e = osc::launch_chain(g, K, threads, stream);
-        if (e != cudaSuccess)
-            return cuda_fail(e, "chain_rk4_kernel");
-        if (es && (k0 + n) % stride == 0) {
-            e = osc::launch_energy(m, C, nx, nv, es + ((k0 + n) / stride) * B, B, s, false,
-                                   stream);
+
+    // The time loop over chains [b0, b0 + nb) on stream st.
+    auto run_group = [&](int64_t b0, int64_t nb, cudaStream_t st) -> int {
+        const int64_t o = b0 * s;
+        osc::SegArgs gg = g;
+        gg.m = m + o;
+        gg.C = C + o;
+        gg.first_bad = first_bad + b0;
+        gg.nbuf = nb;
+        double *cx = x + o, *cv = v + o, *nx = scratch.p + o, *nv = scratch.p + cells + o;
+        for (int64_t k0 = 0; k0 < nsteps;) {
+            int64_t n = nsteps - k0;
+            if (n > per_launch)
+                n = per_launch;
+            const int64_t next_sample = (k0 / stride + 1) * stride;
+            if (next_sample - k0 < n)
+                n = next_sample - k0;
+            gg.xin = cx;
+            gg.vin = cv;
+            gg.xout = nx;
+            gg.vout = nv;
+            gg.nsteps = n;
+            gg.step0 = k0;
+            const bool sample = xs && (k0 + n) % stride == 0;
+            gg.xs = sample ? xs + ((k0 + n) / stride) * cells + o : nullptr;
+            gg.vs = sample ? vs + ((k0 + n) / stride) * cells + o : nullptr;
+            cudaError_t e = osc::launch_chain(gg, K, threads, st);
             if (e != cudaSuccess)
-                return cuda_fail(e, "energy_kernel");
+                return cuda_fail(e, "chain_rk4_kernel");
+            if (es && (k0 + n) % stride == 0) {
+                e = osc::launch_energy(gg.m, gg.C, nx, nv, es + ((k0 + n) / stride) * B + b0, nb,
+                                       s, false, st);
+                if (e != cudaSuccess)
+                    return cuda_fail(e, "energy_kernel");
+            }
+            std::swap(cx, nx);
+            std::swap(cv, nv);
+            k0 += n;
         }
-        std::swap(cx, nx);
-        std::swap(cv, nv);
-        k0 += n;
-    }
-    if (cx != x) {
-        OSC_CUDA(cudaMemcpyAsync(x, cx, bytes, cudaMemcpyDeviceToDevice, stream));
-        OSC_CUDA(cudaMemcpyAsync(v, cv, bytes, cudaMemcpyDeviceToDevice, stream));
-    }
-    return OSC_OK;
+        if (cx != x + o) {
+            const size_t gb = sizeof(double) * static_cast<size_t>(nb * s);
+            OSC_CUDA(cudaMemcpyAsync(x + o, cx, gb, cudaMemcpyDeviceToDevice, st));
+            OSC_CUDA(cudaMemcpyAsync(v + o, cv, gb, cudaMemcpyDeviceToDevice, st));
+        }
+        return OSC_OK;
+    };
+
+    // Whole-chain batches of many waves run as two independent halves on two
+    // streams, so that one half's launches fill the other's tail wave
+    // (chains are independent: same bytes either way).
+    if (!(plan.tiles == 1 && B >= kSplitChains))
+        return run_group(0, B, stream);
+    cudaStream_t side = nullptr;
+    OSC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    struct SideStream {
+        cudaStream_t s;
+        ~SideStream() { cudaStreamDestroy(s); }
+    } side_guard{side};
+    cudaEvent_t fork, join;
+    OSC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    OSC_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    struct Events {
+        cudaEvent_t a, b;
+        ~Events()
+        {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } ev_guard{fork, join};
+    OSC_CUDA(cudaEventRecord(fork, stream));
+    OSC_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    const int64_t half = B / 2;
+    int rc = run_group(0, half, stream);
+    const int rc2 = run_group(half, B - half, side);
+    OSC_CUDA(cudaEventRecord(join, side));
+    OSC_CUDA(cudaStreamWaitEvent(stream, join, 0));  // also orders the scratch free
+    if (rc == OSC_OK)
+        rc = rc2;
+    return rc;
 }
 
 int osc_chain_plan(int64_t B, int64_t s, int64_t nsteps, int64_t halo_steps, int64_t *plan)

@@ -161,3 +161,28 @@ def test_divergence_step_not_lost_to_tile_order():
                                          sample=False)
     assert 32 < fb[0] <= 64
     assert int(res.first_bad[0]) == int(fb[0])
+
+
+def test_whole_chain_batch_split_over_two_streams():
+    """>= 1024 whole chains run as two halves on two streams: samples,
+    energies, final states and per-chain divergence steps (one diverging
+    chain in each half) equal the oracle's."""
+    B, s = 1500, 64
+    rng = np.random.default_rng(33)
+    m = rng.uniform(0.5, 2.0, (B, s))
+    C = rng.uniform(500.0, 2000.0, (B, s))
+    x0 = rng.standard_normal((B, s))
+    v0 = rng.standard_normal((B, s))
+    C[100, 30] = 3e8   # first half diverges
+    C[1400, 5] = 5e8   # second half diverges
+    res = batched.integrate_chains(m, C, x0, v0, 1e-3, 600, 150, sample=True, energies=True,
+                                   check=False)
+    xs, vs, xo, vo, fb = oracle.c_rk4_chains(m, C, x0, v0, 1e-3, 600, 150)
+    assert res.first_bad.cpu().numpy().tolist() == fb.tolist()
+    assert fb[100] > 0 and fb[1400] > 0
+    ok = fb == 0
+    assert bits(res.xs.cpu().numpy()[:, ok]) == bits(xs[:, ok])
+    assert bits(res.x.cpu().numpy()[ok]) == bits(xo[ok])
+    es = res.energies.cpu().numpy()
+    for k in range(xs.shape[0]):
+        assert bits(es[k][ok]) == bits(oracle.c_energy(m[ok], C[ok], xs[k][ok], vs[k][ok]))

@@ -520,8 +520,11 @@ int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, d
     cudaError_t e = osc::launch_dense_pack(X, V, BA, Vp, s, N, sp, Np, k.half_dt, stream);
     if (e != cudaSuccess)
         return cuda_fail(e, "pack_kernel");
+    cudaStream_t side = nullptr;
+    OSC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     e = osc::launch_dense_steps(Ause, BA, BB, Vp, SX, SV, first_bad, sp, Np, k, 0, nsteps,
-                                stream);
+                                stream, side);
+    cudaStreamDestroy(side);  // released once its queued work is done
     if (e != cudaSuccess)
         return cuda_fail(e, "dense_rk4_gemm");
     e = osc::launch_dense_unpack(BA, Vp, X, V, s, N, Np, stream);

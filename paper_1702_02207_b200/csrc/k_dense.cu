@@ -80,6 +80,7 @@ struct DenseArgs {
     int64_t s, N;      // padded sizes: s % 64 == 0, N % TB == 0
     StepConsts k;
     int64_t step;      // 1-based step index (divergence tag)
+    int64_t nt0, ntc;  // column tiles [nt0, nt0 + ntc) of this launch (independent trajectories)
 };
 
 // Per-thread cp.async plan: the global source of each 16-byte chunk this
@@ -132,9 +133,8 @@ __global__ void __launch_bounds__(THREADS, 4) dense_rk4_gemm(DenseArgs g)
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;  // 2 x 2 warps of 32 x 16
-    const int64_t ntn = (2 * g.N) / BN;
-    const int64_t m0 = static_cast<int64_t>(blockIdx.x / ntn) * BM;
-    const int64_t n0 = static_cast<int64_t>(blockIdx.x % ntn) * BN;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x / g.ntc) * BM;
+    const int64_t n0 = (g.nt0 + static_cast<int64_t>(blockIdx.x % g.ntc)) * BN;
     const int64_t KT = g.s / BK;
 
     double acc[4][2][2];
@@ -313,7 +313,8 @@ cudaError_t launch_rowscale(const double *K, const double *m, double *A, int64_t
 // Integrate nsteps with the padded workspace already holding the packed state.
 cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *Vp, double *SX,
                                double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
-                               StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream)
+                               StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream,
+                               cudaStream_t side)
 {
     DenseArgs g{};
     g.A = A;
@@ -330,22 +331,51 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
                          static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(dense_rk4_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
-    const unsigned blocks = static_cast<unsigned>((sp / BM) * ((2 * Np) / BN));
+    const int64_t ntn = (2 * Np) / BN;  // column tiles
     if (std::getenv("OSC_DENSE_RAW")) {  // benchmark-only: GEMMs without the RK4 epilogue
         cudaFuncSetAttribute(dense_rk4_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSmemBytes));
+        g.nt0 = 0;
+        g.ntc = ntn;
+        const unsigned blocks = static_cast<unsigned>((sp / BM) * ntn);
         for (int64_t t = 0; t < 2 * nsteps; ++t) {
             g.Bop = BA;
             dense_rk4_gemm<2><<<blocks, THREADS, kSmemBytes, stream>>>(g);
         }
         return cudaGetLastError();
     }
-    for (int64_t t = 0; t < nsteps; ++t) {
-        g.step = step0 + t + 1;
-        g.Bop = BA;
-        dense_rk4_gemm<0><<<blocks, THREADS, kSmemBytes, stream>>>(g);
-        g.Bop = BB;
-        dense_rk4_gemm<1><<<blocks, THREADS, kSmemBytes, stream>>>(g);
+    // Trajectories (column blocks) are independent, so wide batches run as two
+    // halves of column tiles on two streams: each half's launches fill the
+    // other's tail wave (4096 CTAs = 6.92 waves of 592 at C5).  Same bytes.
+    const int nhalf = (side && ntn >= 16) ? 2 : 1;
+    cudaStream_t streams[2] = {stream, side};
+    int64_t begin[2] = {0, ntn / 2}, count[2] = {ntn, ntn - ntn / 2};
+    if (nhalf == 2)
+        count[0] = ntn / 2;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (nhalf == 2) {
+        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+        cudaEventRecord(fork, stream);
+        cudaStreamWaitEvent(side, fork, 0);
+    }
+    for (int h = 0; h < nhalf; ++h) {
+        g.nt0 = begin[h];
+        g.ntc = count[h];
+        const unsigned blocks = static_cast<unsigned>((sp / BM) * g.ntc);
+        for (int64_t t = 0; t < nsteps; ++t) {
+            g.step = step0 + t + 1;
+            g.Bop = BA;
+            dense_rk4_gemm<0><<<blocks, THREADS, kSmemBytes, streams[h]>>>(g);
+            g.Bop = BB;
+            dense_rk4_gemm<1><<<blocks, THREADS, kSmemBytes, streams[h]>>>(g);
+        }
+    }
+    if (nhalf == 2) {
+        cudaEventRecord(join, side);
+        cudaStreamWaitEvent(stream, join, 0);
+        cudaEventDestroy(fork);
+        cudaEventDestroy(join);
     }
     return cudaGetLastError();
 }

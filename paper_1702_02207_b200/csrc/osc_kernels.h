@@ -84,7 +84,8 @@ cudaError_t launch_dense_pack(const double *X, const double *V0, double *BA, dou
                               cudaStream_t stream);
 cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *Vp, double *SX,
                                double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
-                               StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream);
+                               StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream,
+                               cudaStream_t side = nullptr);
 cudaError_t launch_dense_unpack(const double *BA, const double *Vp, double *X, double *V,
                                 int64_t s, int64_t N, int64_t Np, cudaStream_t stream);
 

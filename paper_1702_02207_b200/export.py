@@ -63,7 +63,8 @@ def integrate_chains_to_npy(m, C, x0, v0, dt, nsteps, stride, path_prefix, *, ha
 
     Writes ``<prefix>.x.npy`` and ``<prefix>.v.npy`` ([1+nsteps//stride][B][s])
     and ``<prefix>.t.npy`` (accumulated time labels).  Returns the 1-based
-    first bad step per chain (samples after it are not written).
+    first bad step per chain (0: none); a diverged chain's samples after that
+    step are unspecified, as integrate would have raised there.
     """
     import torch
 
@@ -84,7 +85,7 @@ def integrate_chains_to_npy(m, C, x0, v0, dt, nsteps, stride, path_prefix, *, ha
     host = [(torch.empty((B, s), dtype=torch.float64).pin_memory(),
              torch.empty((B, s), dtype=torch.float64).pin_memory()) for _ in range(2)]
     done = [None, None]
-    first_bad = torch.zeros(B, dtype=torch.int64)
+    first_bad = torch.zeros(B, dtype=torch.int64, device=m.device)  # stays on the device
 
     def flush(slot, j):
         done[slot].synchronize()
@@ -112,8 +113,9 @@ def integrate_chains_to_npy(m, C, x0, v0, dt, nsteps, stride, path_prefix, *, ha
     j = 0
     while k < nsteps:
         n = min(stride, nsteps - k)
-        res = batched.integrate_chains(m, C, x, v, dt, n, check=False, halo_steps=halo_steps)
-        fb = res.first_bad.cpu()
+        res = batched.integrate_chains(m, C, x, v, dt, n, check=False, halo_steps=halo_steps,
+                                       validate=(k == 0))
+        fb = res.first_bad  # no host sync: the next interval queues behind this one
         first_bad = torch.where((first_bad == 0) & (fb > 0), fb + k, first_bad)
         x, v = res.x, res.v
         k += n
@@ -126,4 +128,4 @@ def integrate_chains_to_npy(m, C, x0, v0, dt, nsteps, stride, path_prefix, *, ha
             done[jj % 2] = None
     fx.flush()
     fv.flush()
-    return first_bad.numpy()
+    return first_bad.cpu().numpy()

@@ -86,10 +86,16 @@ def test_local_group_peer_transport_divergence():
 
 # property-based: random chain lengths, shard counts, steps per period and
 # transports all give the single-GPU bytes (parallel.py:11-14's contract)
+import os as _os
 from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
 
+_SOAK = int(_os.environ.get("HYPOTHESIS_SOAK", "1"))  # bug-hunt scaling (scripts/)
+# the default run replays a fixed example set (reproducible suite); a soak
+# (scripts/hypothesis_soak.sh) explores fresh random examples
+_DERANDOMIZE = _SOAK == 1
 
-@settings(max_examples=100, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+
+@settings(max_examples=100 * _SOAK, deadline=None, derandomize=_DERANDOMIZE, suppress_health_check=[HealthCheck.too_slow])
 @given(s=st.integers(2_000, 60_000), shards=st.integers(1, 8), T=st.integers(1, 40),
        nsteps=st.integers(1, 150), transport=st.sampled_from(["nccl", "peer"]),
        seed=st.integers(0, 2**32 - 1))
@@ -131,7 +137,7 @@ def test_c_entry_sharded_chain_divergence():
     assert e.value.step == int(ref.first_bad[0]) > 0
 
 
-@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@settings(max_examples=40 * _SOAK, deadline=None, derandomize=_DERANDOMIZE, suppress_health_check=[HealthCheck.too_slow])
 @given(s=st.integers(2_000, 40_000), shards=st.integers(1, 6), T=st.integers(1, 40),
        nsteps=st.integers(1, 120), seed=st.integers(0, 2**32 - 1))
 def test_c_entry_sharded_random(s, shards, T, nsteps, seed):

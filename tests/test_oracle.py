@@ -156,7 +156,7 @@ _REF = "/root/reference/pkg/src"
 
 
 @pytest.mark.skipif(not os.path.isdir(_REF), reason="reference package not present")
-@settings(max_examples=40, deadline=None)
+@settings(max_examples=40, deadline=None, derandomize=True)
 @given(s=st.integers(1, 9), nsteps=st.integers(1, 60), stride=st.integers(1, 7),
        seed=st.integers(0, 2**32 - 1), dt=st.sampled_from([1e-4, 1e-3, 5e-3, 2e-2]))
 def test_c_oracle_equals_reference_on_random_chains(s, nsteps, stride, seed, dt):

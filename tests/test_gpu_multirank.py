@@ -79,3 +79,23 @@ def test_processes_report_first_divergence(transport):
     fb, _, _ = _run(2, s, 300, 32, stiff=50_000, transport=transport)
     ref = batched.integrate_chains(*_chain(s, 21, 50_000), 1e-3, 300, check=False)
     assert fb > 0 and fb == int(ref.first_bad[0])
+
+
+# random decompositions across real processes (a fixed example set by
+# default; scripts/hypothesis_soak.sh with HYPOTHESIS_SOAK explores more)
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+_SOAK = int(os.environ.get("HYPOTHESIS_SOAK", "1"))
+
+
+@settings(max_examples=3 * _SOAK, deadline=None, derandomize=_SOAK == 1,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(world=st.integers(2, 3), s=st.integers(20_000, 150_000), T=st.integers(4, 40),
+       nsteps=st.integers(1, 130), transport=st.sampled_from(["nccl", "peer"]))
+def test_processes_random_decompositions(world, s, T, nsteps, transport):
+    from paper_1702_02207_b200 import batched
+
+    fb, x, v = _run(world, s, nsteps, T, transport=transport)
+    ref = batched.integrate_chains(*_chain(s, 21), 1e-3, nsteps)
+    assert fb == 0
+    assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())

@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 7
+#define OSC_ABI_VERSION 8
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -138,6 +138,16 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
                           int64_t step0, int64_t *first_bad, const osc_peer_t *left,
                           const osc_peer_t *right, uint32_t flags, void *stream);
+
+/* Stream-ordered 64-bit counters, for ordering work across processes
+ * without host synchronisation: osc_stream_write_u64 stores value at addr
+ * once all prior work of stream is done (preceded by a system-scope fence, so
+ * a kernel's peer-memory stores are visible first); osc_stream_wait_u64 holds
+ * later work of stream until (int64_t)(*addr - value) >= 0.  The wait is
+ * done by the GPU front-end -- no kernel spins.  addr: device memory of this
+ * process or a peer's, mapped with osc_ipc_import. */
+int osc_stream_write_u64(void *stream, void *addr, uint64_t value);
+int osc_stream_wait_u64(void *stream, const void *addr, uint64_t value);
 
 /* One chain of s cells sharded over the GPUs of THIS process (devs[ngpu],
  * ids may repeat), host buffers m, C, x, v [s] (x, v updated in place),

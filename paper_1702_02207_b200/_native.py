@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
-ABI_VERSION = 7
+ABI_VERSION = 8
 OSC_FMA = 1
 
 _i64 = ctypes.c_int64
@@ -38,6 +38,8 @@ SIGNATURES = {
     "osc_rk4_chain_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                              _dbl, _i64, _i64, _vp, _vp, _vp, ctypes.c_uint32,
                                              _vp]),
+    "osc_stream_write_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
+    "osc_stream_wait_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_chain_plan": (ctypes.c_int, [_i64, _i64, _i64, _i64, _vp]),
     "osc_rk4_chain_sharded": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), _vp,
                                              _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,

@@ -10,6 +10,8 @@
 #include <utility>
 #include <vector>
 
+#include <cuda.h>  // driver types only: entry points via cudaGetDriverEntryPoint
+
 #include "../../include/osc_b200.h"
 #include "osc_kernels.h"
 
@@ -824,6 +826,70 @@ int osc_rk4_chains_host(const double *m, const double *C, double *x, double *v, 
                         double *vs, int64_t *first_bad)
 {
     return host_run(true, m, C, x, v, B, s, dt, nsteps, stride, xs, vs, first_bad);
+}
+
+// ---------------------------------------------------------------------------
+// Stream-ordered 64-bit counters (cross-process ordering in the GPU front-end)
+// ---------------------------------------------------------------------------
+namespace {
+
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+// Driver entry points resolved through the runtime, so the library does not
+// link libcuda (it must load on machines without a driver for the CPU tests).
+StreamValueFn driver_fn(const char *name)
+{
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return reinterpret_cast<StreamValueFn>(p);
+}
+
+}  // namespace
+
+int osc_stream_write_u64(void *stream, void *addr, uint64_t value)
+{
+    static const StreamValueFn f = driver_fn("cuStreamWriteValue64");
+    if (!addr)
+        return fail(OSC_INVALID, "null counter");
+    if (!f)
+        return fail(OSC_CUDA_ERROR, "cuStreamWriteValue64 is not available");
+    // default flags: a system-scope fence orders all prior work of the stream
+    // (the kernel's peer stores included) before the store
+    const CUresult r = f(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                         CU_STREAM_WRITE_VALUE_DEFAULT);
+    return r == CUDA_SUCCESS ? OSC_OK
+                             : fail(OSC_CUDA_ERROR, "cuStreamWriteValue64 failed (%d)", int(r));
+}
+
+int osc_stream_wait_u64(void *stream, const void *addr, uint64_t value)
+{
+    static const StreamValueFn f = driver_fn("cuStreamWaitValue64");
+    static int flush = -1;  // does the device take CU_STREAM_WAIT_VALUE_FLUSH?
+    if (!addr)
+        return fail(OSC_INVALID, "null counter");
+    if (!f)
+        return fail(OSC_CUDA_ERROR, "cuStreamWaitValue64 is not available");
+    const CUstream st = static_cast<CUstream>(stream);
+    const CUdeviceptr a = reinterpret_cast<CUdeviceptr>(addr);
+    if (flush != 0) {
+        // GEQ + flush of outstanding remote (peer) writes into this device
+        const CUresult r = f(st, a, value, CU_STREAM_WAIT_VALUE_GEQ | CU_STREAM_WAIT_VALUE_FLUSH);
+        if (r == CUDA_SUCCESS) {
+            flush = 1;
+            return OSC_OK;
+        }
+        if (flush == 1)
+            return fail(OSC_CUDA_ERROR, "cuStreamWaitValue64 failed (%d)", int(r));
+        flush = 0;  // not supported here: plain GEQ (the writer's fence orders its stores)
+    }
+    const CUresult r = f(st, a, value, CU_STREAM_WAIT_VALUE_GEQ);
+    return r == CUDA_SUCCESS ? OSC_OK
+                             : fail(OSC_CUDA_ERROR, "cuStreamWaitValue64 failed (%d)", int(r));
 }
 
 // ---------------------------------------------------------------------------

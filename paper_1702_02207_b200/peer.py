@@ -93,3 +93,17 @@ class IpcEvent:
         if self.ev:
             _check(_native.lib().osc_event_destroy(ctypes.c_void_p(self.ev)), "osc_event_destroy")
             self.ev = 0
+
+
+def stream_write_u64(stream: torch.cuda.Stream, ptr: int, value: int):
+    """Store value at ptr once all prior work of stream is done (fenced)."""
+    _check(_native.lib().osc_stream_write_u64(ctypes.c_void_p(stream.cuda_stream),
+                                              ctypes.c_void_p(ptr), int(value)),
+           "osc_stream_write_u64")
+
+
+def stream_wait_u64(stream: torch.cuda.Stream, ptr: int, value: int):
+    """Hold later work of stream until *ptr >= value (GPU front-end wait)."""
+    _check(_native.lib().osc_stream_wait_u64(ctypes.c_void_p(stream.cuda_stream),
+                                             ctypes.c_void_p(ptr), int(value)),
+           "osc_stream_wait_u64")

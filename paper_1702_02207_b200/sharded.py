@@ -21,12 +21,14 @@ Two transports:
   state buffers (CUDA IPC; NVLink peer memory between GPUs) and the tile
   kernel itself stores its boundary cells into the neighbours' next-input
   ghost zones (``osc_peer_t``), so there is no exchange step at all.  Order is
-  kept with device-side dependencies only: a rank's period-p launch waits
-  (``cudaStreamWaitEvent`` on interprocess events) for its neighbours'
-  period-(p-1) launches, which both produced its ghosts and finished reading
-  the buffer it is about to write into (ping-pong buffers).  A host barrier on
-  a gloo group orders event records before waits; the GPUs never wait on one
-  another inside a kernel.
+  kept on the device only: after its period-p launch a rank's stream stores
+  p + 1 into its period counter (``osc_stream_write_u64``, fenced after the
+  kernel's peer stores), and before period p its stream waits until each
+  neighbour's counter reaches p (``osc_stream_wait_u64``) -- the neighbour's
+  period p-1 both produced our ghosts and finished reading the buffer we are
+  about to write into (ping-pong buffers, parity from the global period
+  count).  The waits happen in the GPU front-end: no host barrier per period,
+  and no kernel ever waits on another GPU.
 """
 
 from __future__ import annotations
@@ -137,8 +139,10 @@ class ShardedChain:
 
     # -- fused exchange over peer memory --------------------------------------
     def peer_descriptors(self, p):
-        """(left, right) osc_peer_t tuples for period p: the neighbours' buffer
-        (p+1) % 2 -- the one they read next period -- and our cell offsets."""
+        """(left, right) osc_peer_t tuples for GLOBAL period p (counted over all
+        runs since setup, so the ping-pong parity stays right across runs with
+        an odd number of periods): the neighbours' buffer (p+1) % 2 -- the one
+        they read next period -- and our cell offsets."""
         g = self.L.g
         out = []
         for nb in (self.rank - 1, self.rank + 1):
@@ -152,35 +156,40 @@ class ShardedChain:
         return tuple(out)
 
     def _setup_peer(self):
-        """Own state in exportable allocations; map the neighbours' state buffers
-        and events (CUDA IPC: NVLink peer memory between GPUs)."""
+        """Own state and period counter in exportable allocations; map the
+        neighbours' (CUDA IPC: NVLink peer memory between GPUs)."""
         from . import peer
 
         self.host_group = dist.new_group(backend="gloo")
+        self.peer_counters = {}
         n = self.L.n
         self._own = [peer.DeviceVector(n, self.device) for _ in range(4)]
         for dst, src in zip(self._own, (self.x, self.v, self.x2, self.v2)):
             dst.tensor.copy_(src)
         self.x, self.v, self.x2, self.v2 = (b.tensor for b in self._own)
-        self.events = [peer.IpcEvent() for _ in range(2)]
+        # period counter: our stream stores p + 1 after our period p; the
+        # neighbours' streams wait on it (no host barrier per period)
+        self._counter = peer.DeviceVector(1, self.device)
+        self._counter.tensor.zero_()
+        self._period = 0
         torch.cuda.synchronize(self.device)
         mine = {"blo": self.L.blo, "bufs": [b.handle() for b in self._own],
-                "events": [e.handle for e in self.events]}
+                "counter": self._counter.handle()}
         infos = [None] * self.world
         dist.all_gather_object(infos, mine, group=self.host_group)
-        self.peer_events = {}
         self._imported = []
         for nb in (self.rank - 1, self.rank + 1):
             if 0 <= nb < self.world:
                 ptrs = [peer.import_buffer(h) for h in infos[nb]["bufs"]]
                 self._imported += ptrs
                 self.peer_bufs[nb] = (((ptrs[0], ptrs[1]), (ptrs[2], ptrs[3])), infos[nb]["blo"])
-                self.peer_events[nb] = [peer.IpcEvent(h) for h in infos[nb]["events"]]
+                self.peer_counters[nb] = peer.import_buffer(infos[nb]["counter"])
+                self._imported.append(self.peer_counters[nb])
 
     def close(self):
         """Release peer resources in a safe order: finish local work, unmap the
-        neighbours' buffers and close their events, wait until every rank has
-        done so, then free the buffers and events this rank exported."""
+        neighbours' buffers and counters, wait until every rank has done so,
+        then free the allocations this rank exported."""
         if not getattr(self, "_own", None):
             return
         from . import peer
@@ -189,10 +198,7 @@ class ShardedChain:
         dist.barrier(group=self.host_group)  # no rank still writes into anyone
         for ptr in self._imported:
             peer.close_buffer(ptr)
-        for evs in self.peer_events.values():
-            for ev in evs:
-                ev.destroy()
-        self._imported, self.peer_events = [], {}
+        self._imported, self.peer_counters = [], {}
         self.peer_bufs.clear()
         dist.barrier(group=self.host_group)  # every mapping of our memory is gone
         # keep the results readable: move them to ordinary tensors first
@@ -201,8 +207,7 @@ class ShardedChain:
         torch.cuda.synchronize(self.device)
         for b in self._own:
             b.free()
-        for ev in self.events:
-            ev.destroy()
+        self._counter.free()
         self._own = []
 
     def __enter__(self):
@@ -212,27 +217,34 @@ class ShardedChain:
         self.close()
 
     def _run_peer(self, nsteps):
+        """Fused exchange, ordered on the device: before period q (a running
+        count over runs) our stream waits until each neighbour's counter shows
+        its period q-1 done -- it produced our ghosts and finished reading the
+        buffer we now store into (ping-pong) -- and after our launch it stores
+        q + 1 into our counter.  The waits happen in the GPU front-end; no
+        kernel ever spins on another GPU and no host barrier is needed."""
+        from . import peer
+
         main = torch.cuda.current_stream(self.device)
         a, b = self.L.own
-        k = p = 0
+        k = 0
         while k < nsteps:
             n = min(self.T, nsteps - k)
-            if p > 0:  # neighbours' period p-1 wrote our ghosts and left their buffer
-                for evs in self.peer_events.values():
-                    evs[(p - 1) % 2].wait(main)
-            left, right = self.peer_descriptors(p)
+            q = self._period
+            for ptr in self.peer_counters.values():
+                peer.stream_wait_u64(main, ptr, q)
+            left, right = self.peer_descriptors(q)
             self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, k,
                          self.first_bad, left=left, right=right)
-            self.events[p % 2].record(main)
-            dist.barrier(group=self.host_group)  # every period-p record precedes any wait
+            peer.stream_write_u64(main, self._counter.ptr, q + 1)
             self.x, self.x2 = self.x2, self.x
             self.v, self.v2 = self.v2, self.v
+            self._period += 1
             k += n
-            p += 1
         # neighbours' final writes land only in ghost zones; our owned cells are
         # complete on our stream.  Make sure no peer kernel still targets us.
-        for evs in self.peer_events.values():
-            evs[(p - 1) % 2].wait(main)
+        for ptr in self.peer_counters.values():
+            peer.stream_wait_u64(main, ptr, self._period)
 
     # -- ghost exchange ------------------------------------------------------
     def boundary(self, x, v):
@@ -392,6 +404,7 @@ class LocalShardGroup:
         self.parts = [ShardedChain(m, C, x0, v0, dt, halo_steps=halo_steps, device=device,
                                    advance=advance, rank=r, world=shards)
                       for r in range(shards)]
+        self._period = 0
         if transport == "peer":  # neighbours' buffers are plain local tensors here
             for r, p in enumerate(self.parts):
                 for nb in (r - 1, r + 1):
@@ -403,9 +416,10 @@ class LocalShardGroup:
         """Fused exchange, all shards on one stream: stream order is the only
         synchronisation needed."""
         T = self.parts[0].T
-        k = p = 0
+        k = 0
         while k < nsteps:
             n = min(T, nsteps - k)
+            p = self._period  # global: the ping-pong parity carries over runs
             for sh in self.parts:
                 a, b = sh.L.own
                 left, right = sh.peer_descriptors(p)
@@ -415,7 +429,7 @@ class LocalShardGroup:
                 sh.x, sh.x2 = sh.x2, sh.x
                 sh.v, sh.v2 = sh.v2, sh.v
             k += n
-            p += 1
+            self._period += 1
 
     def run(self, nsteps: int) -> int:
         if self.transport == "peer":

@@ -99,3 +99,37 @@ def test_processes_random_decompositions(world, s, T, nsteps, transport):
     ref = batched.integrate_chains(*_chain(s, 21), 1e-3, nsteps)
     assert fb == 0
     assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
+
+
+
+def _worker_runs(rank, world, port, s, runs, T, transport, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1702_02207_b200 import sharded
+
+        sh = sharded.ShardedChain(*_chain(s, 21), 1e-3, halo_steps=T, transport=transport)
+        fb = 0
+        for n in runs:
+            fb = fb or sh.run(n)
+        x, v = sh.gather()
+        sh.close()
+        if rank == 0:
+            q.put((fb, x.numpy(), v.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_processes_several_runs_with_odd_periods(transport):
+    """Consecutive run() calls of 3, 5 and 1 periods (the bench calls run()
+    once per timed step) equal one run of the total steps, byte for byte."""
+    from paper_1702_02207_b200 import batched
+
+    s, T = 90_000, 16
+    runs = (3 * T, 5 * T, T - 5)
+    fb, x, v = collect(_worker_runs, (2, _port(), s, runs, T, transport), 2)
+    ref = batched.integrate_chains(*_chain(s, 21), 1e-3, sum(runs))
+    assert fb == 0
+    assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())

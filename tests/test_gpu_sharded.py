@@ -148,3 +148,18 @@ def test_c_entry_sharded_random(s, shards, T, nsteps, seed):
                                            halo_steps=T)
     ref = batched.integrate_chains(m, C, x0, v0, 1e-3, nsteps)
     assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
+
+
+def test_peer_transport_across_runs_with_odd_periods():
+    """Regression: the fused peer exchange picks the neighbours' next-input
+    buffer by period parity; that parity must carry over run() calls (an odd
+    number of periods per run flips the ping-pong)."""
+    s, T = 60_000, 8
+    m, C, x0, v0 = _chain(s, 77)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 3, halo_steps=T, transport="peer")
+    for n in (3 * T, 5 * T + 3, T, 2 * T):  # 3, 6, 1, 2 periods
+        assert grp.run(n) == 0
+    x, v = grp.gather()
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 3 * T + 5 * T + 3 + T + 2 * T)
+    assert bits(x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
+    assert bits(v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())

@@ -1,0 +1,206 @@
+// Internal helpers shared by the C-ABI translation units (capi*.cu): the
+// per-thread last error, argument checks the reference makes, the chain
+// launch plan, stream-ordered scratch.  Not part of the public ABI
+// (include/osc_b200.h is).
+#pragma once
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <algorithm>
+#include <utility>
+#include <vector>
+
+#include "../../include/osc_b200.h"
+#include "osc_kernels.h"
+
+namespace osc_capi {
+
+inline thread_local std::string g_last_error;  // one per thread, shared by every capi_*.cu
+
+inline int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+inline int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+inline int cuda_fail(cudaError_t e, const char *where)
+{
+    return fail(OSC_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define OSC_CUDA(call)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return cuda_fail(e_, #call);                                                    \
+    } while (0)
+
+// The reference's argument checks: rk4_step's dt (oscillator.py:201-202) and
+// integrate's nsteps/stride (oscillator.py:247-250).
+inline int check_run_args(double dt, int64_t nsteps, int64_t stride)
+{
+    if (!(std::isfinite(dt) && dt > 0.0))
+        return fail(OSC_INVALID, "dt must be positive and finite, got %.17g", dt);
+    if (nsteps < 1)
+        return fail(OSC_INVALID, "nsteps must be >= 1, got %lld", (long long)nsteps);
+    if (stride < 1)
+        return fail(OSC_INVALID, "stride must be >= 1, got %lld", (long long)stride);
+    return OSC_OK;
+}
+
+inline osc::StepConsts consts(double dt)
+{
+    // Exactly the reference's constants: half_dt = 0.5 * dt (oscillator.py:208)
+    // and dt / 6.0 inside combine_value (oscillator.py:174).
+    return osc::StepConsts{dt, 0.5 * dt, dt / 6.0};
+}
+
+constexpr int64_t kWholeChainMax = 2048;  // 256 threads x 8 cells
+constexpr int64_t kWholeChainSteps = 512; // steps per launch in whole-chain mode
+constexpr int64_t kSplitChains = 1024;     // whole-chain batches this large run as two halves
+// Tiled shape, measured on B200 for s = 2^24 (profiles/r01/README.md): with
+// the persistent prefetching kernel, 8 cells x 256 threads and 32-step halos
+// beat 8 x 128 at T = 16..24 by 3-8% and 4 x 256 / 4 x 512 by 12-14%.
+constexpr int kTileK = 8, kTileThreads = 256;
+constexpr int64_t kTile = int64_t(kTileK) * kTileThreads;
+constexpr int64_t kDefaultHaloSteps = 32;
+
+inline void pick_whole(int64_t s, int &K, int &threads)
+{
+    // Fewest cells per thread that keep the CTA at <= 128 threads, else 256
+    // threads of 8 cells.  Measured on B200 for s = 1024 (profiles/r01
+    // sweep_C4_*): K=8 x 128 threads beats K=4 x 256 by 8% and K=2 x 512 by 2.4x.
+    K = 8;
+    for (int k : {1, 2, 4, 8}) {
+        if ((s + k - 1) / k <= 128) {
+            K = k;
+            break;
+        }
+    }
+    const int64_t t = (s + K - 1) / K;
+    threads = static_cast<int>(((t + 31) / 32) * 32);
+}
+
+// Steps per tiled launch when the caller leaves it to us.  A launch costs
+// rounds(T) tile-times of (T + c) steps, where rounds(T) = ceil(tiles(T) /
+// CTAs) (one persistent CTA per SM) and c ~ 4 steps covers a tile's load,
+// setup and store; per step that is rounds(T) * (T + c) / T.  Deeper halos
+// mean fewer launches but narrower owned tiles, so the tile count can cross
+// a multiple of the CTA count: for C3 (2^24 cells) T = 31 gives 59 rounds
+// instead of 60 (+0.7% measured, profiles/r01/README.md).
+inline int64_t pick_halo_steps(int64_t s, int64_t B, int64_t nsteps)
+{
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        sms = 148;            // no device (planning only): B200
+        cudaGetLastError();   // do not leave the query's error pending
+    }
+    constexpr double c = 4.0;
+    int64_t best = kDefaultHaloSteps;
+    double best_cost = 0.0;
+    for (int64_t T : {int64_t(32), int64_t(31), int64_t(30), int64_t(28)}) {
+        if (T > nsteps && T != kDefaultHaloSteps)
+            continue;
+        const int64_t W = kTile - 4 * T;
+        const int64_t tiles = B * ((s + W - 1) / W);
+        const int64_t rounds = (tiles + sms - 1) / sms;
+        const double cost = double(rounds) * (double(T) + c) / double(T);
+        if (best_cost == 0.0 || cost < best_cost * (1.0 - 1e-9)) {
+            best = T;
+            best_cost = cost;
+        }
+    }
+    return best;
+}
+
+// Tuning hook (benchmarks only): OSC_TILE="K,threads" / OSC_WHOLE="K,threads"
+// override the tiled / whole-chain launch shapes.  Read-only process state.
+inline bool env_shape(const char *name, int &K, int &threads)
+{
+    const char *e = std::getenv(name);
+    int k = 0, t = 0;
+    if (!e || std::sscanf(e, "%d,%d", &k, &t) != 2)
+        return false;
+    if ((k != 1 && k != 2 && k != 4 && k != 8) || t < 32 || t > 1024 || t % 32)
+        return false;
+    K = k;
+    threads = t;
+    return true;
+}
+
+struct ChainPlan {
+    int K = kTileK, threads = kTileThreads;
+    int64_t W = 0, H = 0, tiles = 1, per_launch = 0;
+};
+
+// Launch plan of osc_rk4_chains: whole chains up to kWholeChainMax cells
+// (one CTA per chain, kWholeChainSteps steps per launch), else temporally
+// blocked tiles of K x threads cells, H = 2T halo, T steps per launch.
+inline int plan_chain(int64_t s, int64_t B, int64_t nsteps, int64_t halo_steps, ChainPlan &p)
+{
+    int wk = 0, wt = 0;
+    const bool whole_env = env_shape("OSC_WHOLE", wk, wt) && int64_t(wk) * wt >= s;
+    if (s <= kWholeChainMax || whole_env) {
+        pick_whole(s, p.K, p.threads);
+        if (whole_env) {
+            p.K = wk;
+            p.threads = wt;
+        }
+        p.W = s;
+        p.H = 0;
+        p.tiles = 1;
+        p.per_launch = kWholeChainSteps;
+        return OSC_OK;
+    }
+    const bool shaped = env_shape("OSC_TILE", p.K, p.threads);
+    const int64_t T = halo_steps > 0 ? halo_steps
+                                     : (shaped ? kDefaultHaloSteps : pick_halo_steps(s, B, nsteps));
+    p.H = 2 * T;
+    p.W = int64_t(p.K) * p.threads - 2 * p.H;
+    if (p.W < 1)
+        return fail(OSC_INVALID, "halo_steps=%lld too deep for a %lld-cell tile", (long long)T,
+                    (long long)p.K * p.threads);
+    p.tiles = (s + p.W - 1) / p.W;
+    p.per_launch = T;
+    return OSC_OK;
+}
+
+// Keep freed stream-ordered allocations in the device's default pool instead
+// of returning them to the driver at every synchronisation (the default
+// release threshold is 0), so repeated host-API calls do not re-map memory.
+inline void retain_pool_memory()
+{
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev)
+        return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
+
+struct Scratch {
+    double *p = nullptr;
+    cudaStream_t s = nullptr;
+    ~Scratch()
+    {
+        if (p)
+            cudaFreeAsync(p, s);
+    }
+};
+
+}  // namespace osc_capi

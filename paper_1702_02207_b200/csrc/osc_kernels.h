@@ -1,4 +1,4 @@
-// Internal launch interface between the C-ABI layer (capi.cu) and kernels.
+// Internal launch interface between the C-ABI layer (capi*.cu) and kernels.
 #pragma once
 
 #include <cstdint>

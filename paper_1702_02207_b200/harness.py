@@ -96,10 +96,17 @@ def _cuda_timer(fn):
     return out, start.elapsed_time(end) * 1e-3
 
 
-def install(oscbench: types.ModuleType, *, integrate=None, timer=None):
+def install(oscbench: types.ModuleType, *, integrate=None, timer=None, reference=False):
     """Route ``gpu*`` scenarios of ``oscbench.harness.BenchRunner`` to the GPU.
 
-    Returns an ``uninstall`` callable restoring the original function.
+    ``reference=True`` also rebinds ``integrate`` where the reference looks it
+    up -- ``oscbench.harness.integrate`` (``BenchRunner.reference``, the CLI's
+    ``integrate`` command cli.py:119-135, the verify items harness.py:829-857)
+    and the package-level ``oscbench.integrate`` / ``oscbench.oscillator.integrate``
+    -- so whole CLI runs use the B200.  The determinism verdict then compares
+    the GPU with itself: use it for throughput, keep the default to validate.
+    ``run_sequential`` (per-step host latency, harness.py:392-405) is never
+    rerouted.  Returns an ``uninstall`` callable restoring every name.
     """
     harness = oscbench.harness
     original = harness.run_parallel
@@ -112,20 +119,35 @@ def install(oscbench: types.ModuleType, *, integrate=None, timer=None):
         return original(system, state0, scenario)
 
     harness.run_parallel = run_parallel_or_gpu
+    rebound = []
+    if reference:
+        if integrate is None:
+            from .oscillator import integrate as gpu_integrate
+        else:
+            gpu_integrate = integrate
+        for mod in (harness, oscbench, oscbench.oscillator):
+            rebound.append((mod, mod.integrate))
+            mod.integrate = gpu_integrate
 
     def uninstall():
         harness.run_parallel = original
+        for mod, fn in rebound:
+            mod.integrate = fn
 
     return uninstall
 
 
 def main(argv=None) -> int:
     """``python -m paper_1702_02207_b200.harness <oscbench CLI args>``: the
-    reference CLI with ``gpu`` scenarios enabled."""
+    reference CLI with ``gpu`` scenarios enabled; with OSC_GPU_REFERENCE=1 the
+    CLI's ``integrate`` command and the cached reference run on the B200 too
+    (``install(reference=True)``)."""
+    import os
+
     import oscbench
     import oscbench.cli
 
-    install(oscbench)
+    install(oscbench, reference=os.environ.get("OSC_GPU_REFERENCE") == "1")
     return oscbench.cli.main(argv)
 
 

@@ -74,3 +74,31 @@ def test_uninstall_restores_parallel_engine():
     assert oscbench.harness.run_parallel is not original
     uninstall()
     assert oscbench.harness.run_parallel is original
+
+
+def test_reference_rebinding_routes_the_cli_integrate_command(tmp_path, capsys):
+    """install(reference=True): the CLI's integrate command (cli.py:119-135,
+    via BenchRunner.reference) calls the injected integrate; uninstall
+    restores every rebound name."""
+    import oscbench.cli
+
+    calls = []
+    ref_integrate = oscbench.harness.integrate
+
+    def fake_integrate(system, state0, dt, nsteps, stride=1):
+        calls.append(nsteps)
+        return ref_integrate(system, state0, dt, nsteps, stride)
+
+    originals = (oscbench.harness.integrate, oscbench.integrate, oscbench.oscillator.integrate)
+    ini = tmp_path / "run.ini"
+    ini.write_text(INI)
+    uninstall = gpu_harness.install(oscbench, integrate=fake_integrate, reference=True,
+                                    timer=lambda fn: (fn(), 1e-3))
+    try:
+        rc = oscbench.cli.main(["integrate", "--config", str(ini)])
+    finally:
+        uninstall()
+    assert rc == 0 and calls == [2000]
+    assert "max_abs_err_m=" in capsys.readouterr().out
+    assert (oscbench.harness.integrate, oscbench.integrate,
+            oscbench.oscillator.integrate) == originals

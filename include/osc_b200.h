@@ -220,7 +220,9 @@ int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches,
  * enqueues one launch of 8 independent DFMA (mode 0) or DADD (mode 1)
  * chains per thread -- *lane_ops (host) = DP lane-instructions executed -- or
  * of 8 independent DMMA.8x8x4 chains per warp (mode 2; mode 3 adds 8 DFMA
- * chains per thread) -- *lane_ops = flops executed.
+ * chains per thread) -- *lane_ops = flops executed.  Modes 4/5/6: ONE
+ * thread running a dependent DFMA/DADD/DMUL chain, sink[0] = its clock64
+ * cycles, *lane_ops = the chain length (latency, not throughput).
  * sink: device scratch of >= 512 doubles. */
 int osc_bench_fp64(int64_t iters, int mode, double *sink, int64_t *lane_ops, void *stream);
 

@@ -107,6 +107,37 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
 // FP64 issue-rate microbenchmark: 8 independent DFMA (mode 0) or DADD
 // (mode 1) chains per thread.  Gives the measured DP-pipe peak the compute
 // roofline of K1/K2 is quoted against (MEASURED_PEAKS.json has no FP64).
+// One thread, one dependent chain: cycles per DFMA (mode 4), DADD (5) or
+// DMUL (6), measured with clock64 around the chain (sink[0] = cycles).
+__global__ void fp64_latency_kernel(int64_t iters, int mode, double *sink)
+{
+    double a = 1.0 + 1e-3 * threadIdx.x;
+    const double b = 0.999999, c = 1e-7;
+    const long long t0 = clock64();
+    if (mode == 4) {
+        for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                a = __fma_rn(a, b, c);
+        }
+    } else if (mode == 5) {
+        for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                a = __dadd_rn(a, c);
+        }
+    } else {
+        for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                a = __dmul_rn(a, b);
+        }
+    }
+    const long long t1 = clock64();
+    sink[0] = static_cast<double>(t1 - t0);
+    sink[1] = a;
+}
+
 __global__ void fp64_peak_kernel(int64_t iters, int mode, double *sink)
 {
     double a[8];
@@ -221,6 +252,11 @@ cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lan
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int blocks = sms * 4, threads = 512;
+    if (mode >= 4) {  // latency: returned count = dependent ops of the one thread
+        fp64_latency_kernel<<<1, 1, 0, stream>>>(iters, mode, sink);
+        *lanes_ops = iters * 16;
+        return cudaGetLastError();
+    }
     if (mode >= 2) {
         // returned count = flops: 512 per DMMA.8x8x4 per warp (+ 2 per DFMA lane in mode 3)
         dmma_peak_kernel<<<blocks, threads, 0, stream>>>(iters, mode, sink);

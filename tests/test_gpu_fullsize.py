@@ -47,3 +47,20 @@ def test_c5_full_run_against_analytic():
     Xa = oracle.dense_analytic(m, K, X0, p.nsteps * p.dt)
     err = np.max(np.abs(res.x.cpu().numpy() - Xa)) / np.max(np.abs(X0))
     assert err <= 1e-8, err
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_c3_full_run_eight_shards_equal_one_gpu(transport):
+    """The full C3 chain in 8 shards (LocalShardGroup: same kernels, layouts
+    and exchange logic as the multi-GPU driver, all on this device), all 10^4
+    steps, byte-equal to the single-GPU run over every cell."""
+    from paper_1702_02207_b200 import sharded
+
+    m, C, x0, v0 = workloads.c3()
+    p = workloads.PARAMS["C3"]
+    ref = batched.integrate_chains(m, C, x0, v0, p.dt, p.nsteps)
+    grp = sharded.LocalShardGroup(m, C, x0, v0, p.dt, 8, transport=transport)
+    assert grp.run(p.nsteps) == 0
+    x, v = grp.gather()
+    assert torch.equal(x.view(torch.int64), ref.x[0].view(torch.int64))
+    assert torch.equal(v.view(torch.int64), ref.v[0].view(torch.int64))

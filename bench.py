@@ -154,6 +154,28 @@ class ClockSampler:
 # workloads: inputs resident in HBM + one "step" of the hot path
 # --------------------------------------------------------------------------
 
+def workload_desc(name: str, world: int = 1, transport: str = "nccl", T=None) -> dict:
+    """The `config` description of a workload (shared by both bench arms)."""
+    if name == "C2":
+        return {"workload": "C2: 2^20 independent 2-DOF systems (eq. 2), SoA [2][B]",
+                "systems_per_gpu": workloads.C2_B}
+    if name == "C4":
+        return {"workload": "C4: 4096 chains x 1024 cells, [B][s]",
+                "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
+    if name == "C3":
+        return {"workload": "C3: one wall-anchored chain of 2^24 cells",
+                "cells": workloads.C3_S, "halo_steps": T,
+                "sharding": f"{world} contiguous shards, 2T-cell ghost zones "
+                            f"refreshed every T steps ({transport})"}
+    if name == "C5":
+        return {"workload": "C5: dense SPD system s=4096, A = M^-1 K, 1024 trajectories",
+                "s": workloads.C5_S, "trajectories_per_gpu": workloads.C5_N,
+                "gemm_per_launch": "4096 x 4096 x 2048 fp64 (DMMA), RK4 epilogue fused"}
+    if name == "C1":
+        return {"workload": "C1: paper 2-DOF system, C/m=1012.5, 10^6 steps (latency)"}
+    raise SystemExit(f"unknown config {name}")
+
+
 class Workload:
     def __init__(self, name, rank, device, halo, world=1, transport="nccl"):
         import torch
@@ -167,14 +189,12 @@ class Workload:
         if name == "C2":
             arrays = workloads.c2(rank=rank)
             self.kernel, self.launches = "batch2_rk4_kernel", 1
-            self.desc = {"workload": "C2: 2^20 independent 2-DOF systems (eq. 2), SoA [2][B]",
-                         "systems_per_gpu": workloads.C2_B}
+            self.desc = workload_desc(name)
         elif name == "C4":
             arrays = workloads.c4(rank=rank)
             self.kernel = "chain_rk4_kernel<8>"
             self.launches = -(-p.nsteps // 512)
-            self.desc = {"workload": "C4: 4096 chains x 1024 cells, [B][s]",
-                         "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
+            self.desc = workload_desc(name)
         elif name == "C3":
             arrays = workloads.c3()
             plan = batched.chain_plan(1, workloads.C3_S, p.nsteps, halo)
@@ -182,10 +202,7 @@ class Workload:
             self.kernel = "chain_tiles_persistent<8,256>"
             self.launches = plan["launches"]
             self.world = world
-            self.desc = {"workload": "C3: one wall-anchored chain of 2^24 cells",
-                         "cells": workloads.C3_S, "halo_steps": T,
-                         "sharding": f"{world} contiguous shards, 2T-cell ghost zones "
-                                     f"refreshed every T steps ({transport})"}
+            self.desc = workload_desc(name, world, transport, T)
             self.shard = None
             if world > 1 and transport == "nccl":
                 self.launches = 3 * self.launches  # interior + 2 edge launches per period
@@ -193,14 +210,12 @@ class Workload:
             arrays = workloads.c5(rank=rank)  # m, K, X0, V0
             self.kernel = "dense_rk4_gemm"
             self.launches = 2 * p.nsteps  # + rowscale, pack, unpack (counted in gpu_launches)
-            self.desc = {"workload": "C5: dense SPD system s=4096, A = M^-1 K, 1024 trajectories",
-                         "s": workloads.C5_S, "trajectories_per_gpu": workloads.C5_N,
-                         "gemm_per_launch": "4096 x 4096 x 2048 fp64 (DMMA), RK4 epilogue fused"}
+            self.desc = workload_desc(name)
         elif name == "C1":
             arrays = workloads.c1()
             arrays = tuple(a[:, None] for a in arrays)
             self.kernel, self.launches = "batch2_rk4_kernel", 1
-            self.desc = {"workload": "C1: paper 2-DOF system, C/m=1012.5, 10^6 steps (latency)"}
+            self.desc = workload_desc(name)
         else:
             raise SystemExit(f"unknown config {name}")
         self.host = arrays
@@ -511,9 +526,14 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if wl_name == "C3" else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy PCG64, workloads.py)",
-        "config": {"workload": wl_name},
+        "config": dict({k: v for k, v in workload_desc(wl_name).items()
+                        if k not in ("halo_steps", "sharding", "gemm_per_launch")}, dt=wl.dt,
+                       nsteps_per_step=wl.nsteps, parallelism=f"{last['cores']} host threads",
+                       arithmetic="IEEE fp64 CPU restatement, byte-identical to "
+                                  "oscbench.integrate"),
         "cpu_baseline": dict(last, value=value),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -61,6 +61,12 @@ extern "C" {
 int osc_abi_version(void);
 const char *osc_last_error(void);
 
+/* Process-wide side effect: entry points that need scratch memory
+ * (osc_rk4_chains, osc_rk4_dense, the *_host forms) allocate it
+ * stream-ordered from the device's default memory pool and raise that pool's
+ * release threshold once per device (cudaMemPoolAttrReleaseThreshold), so
+ * repeated calls reuse the memory instead of re-mapping it. */
+
 /* Batched independent 2-DOF systems (paper eq. 2), SoA layout [2][B]:
  * m, C, x, v hold coordinate 0 of all B systems, then coordinate 1.
  * Replaces integrate() for s = 2 (oscillator.py:234-263).

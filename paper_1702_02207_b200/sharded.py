@@ -33,6 +33,7 @@ Two transports:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -185,6 +186,23 @@ class ShardedChain:
                 self.peer_bufs[nb] = (((ptrs[0], ptrs[1]), (ptrs[2], ptrs[3])), infos[nb]["blo"])
                 self.peer_counters[nb] = peer.import_buffer(infos[nb]["counter"])
                 self._imported.append(self.peer_counters[nb])
+        # Can this system wait on the mapped counters from a stream?  Try a
+        # wait that is already satisfied; every rank adopts host ordering if
+        # any rank cannot (all ranks must order periods the same way).
+        ok = True
+        try:
+            probe = torch.cuda.current_stream(self.device)
+            for ptr in self.peer_counters.values():
+                peer.stream_wait_u64(probe, ptr, 0)
+                peer.stream_write_u64(probe, self._counter.ptr, 0)
+            torch.cuda.synchronize(self.device)
+        except RuntimeError:
+            ok = False
+        if os.environ.get("OSC_PEER_HOST_ORDER") == "1":  # exercise the fallback
+            ok = False
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok, group=self.host_group)
+        self._host_order = not all(oks)
 
     def close(self):
         """Release peer resources in a safe order: finish local work, unmap the
@@ -231,20 +249,38 @@ class ShardedChain:
         while k < nsteps:
             n = min(self.T, nsteps - k)
             q = self._period
-            for ptr in self.peer_counters.values():
-                peer.stream_wait_u64(main, ptr, q)
+            self._order_before(main, q)
             left, right = self.peer_descriptors(q)
             self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, k,
                          self.first_bad, left=left, right=right)
-            peer.stream_write_u64(main, self._counter.ptr, q + 1)
+            self._order_after(main, q)
             self.x, self.x2 = self.x2, self.x
             self.v, self.v2 = self.v2, self.v
             self._period += 1
             k += n
         # neighbours' final writes land only in ghost zones; our owned cells are
         # complete on our stream.  Make sure no peer kernel still targets us.
-        for ptr in self.peer_counters.values():
-            peer.stream_wait_u64(main, ptr, self._period)
+        self._order_before(main, self._period)
+
+    # Period ordering: stream counters when every rank's system takes stream
+    # memory operations on the mapped counters (decided together at setup),
+    # else host ordering -- finish our period, then a host barrier: slower,
+    # equally correct.
+    def _order_before(self, main, q):
+        from . import peer
+
+        if not self._host_order:
+            for ptr in self.peer_counters.values():
+                peer.stream_wait_u64(main, ptr, q)
+
+    def _order_after(self, main, q):
+        from . import peer
+
+        if self._host_order:
+            torch.cuda.synchronize(self.device)  # our period (and its peer stores) done
+            dist.barrier(group=self.host_group)
+        else:
+            peer.stream_write_u64(main, self._counter.ptr, q + 1)
 
     # -- ghost exchange ------------------------------------------------------
     def boundary(self, x, v):

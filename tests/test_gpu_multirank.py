@@ -133,3 +133,18 @@ def test_processes_several_runs_with_odd_periods(transport):
     ref = batched.integrate_chains(*_chain(s, 21), 1e-3, sum(runs))
     assert fb == 0
     assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
+
+
+def test_peer_transport_host_ordering_fallback(monkeypatch):
+    """Where stream waits on the mapped counters are unavailable, every rank
+    orders periods on the host instead (OSC_PEER_HOST_ORDER=1 forces it):
+    same bytes."""
+    from paper_1702_02207_b200 import batched
+
+    monkeypatch.setenv("OSC_PEER_HOST_ORDER", "1")
+    s, T = 90_000, 16
+    runs = (3 * T, T - 5)
+    fb, x, v = collect(_worker_runs, (2, _port(), s, runs, T, "peer"), 2)
+    ref = batched.integrate_chains(*_chain(s, 21), 1e-3, sum(runs))
+    assert fb == 0
+    assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())

@@ -2,7 +2,7 @@
 
 Run in the build container (the reference does not exist on the GPU box):
 
-    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/gen_golden.py [modal]
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/gen_golden.py [modal|c4full]
 
 Every fixture is the output of ``oscbench.integrate`` / ``oscbench.energy`` /
 ``oscbench.derivative`` (oscillator.py:184-276) on the inputs stored beside it,
@@ -178,8 +178,25 @@ def modal_fixture():
          rand_xs=np.stack(xs_all[2:], -1), rand_ts=ts_all[2])
 
 
+def c4_full_fixture():
+    """Two seeded C4 chains (s = 1024) over the FULL 10^4-step horizon of
+    configs[3], sampled every 1000 steps (the reference takes ~40 s/chain):
+    chains 0 and 1 of the full seeded C4 draw."""
+    m, C, x0, v0 = (a[:2].copy() for a in workloads.c4())
+    p = workloads.PARAMS["C4"]
+    xs, vs = [], []
+    for b in range(2):
+        r = run(m[b], C[b], x0[b], v0[b], p.dt, p.nsteps, 1000)
+        xs.append(r["xs"])
+        vs.append(r["vs"])
+    save("c4_full_subset", m=m, C=C, x0=x0, v0=v0, dt=p.dt, nsteps=p.nsteps, stride=1000,
+         xs=np.stack(xs, 1), vs=np.stack(vs, 1), ts=r["ts"])
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["modal"]:
         modal_fixture()
+    elif sys.argv[1:] == ["c4full"]:
+        c4_full_fixture()
     else:
         main()

@@ -73,6 +73,16 @@ def test_c4_subset_chains(golden):
     assert bits(vs) == bits(g["vs"])
 
 
+def test_c4_full_horizon_chains(golden):
+    """Two C4 chains over the full 10^4 steps of configs[3], sampled every
+    1000 steps, as the reference computed them."""
+    g = golden("c4_full_subset")
+    xs, vs, x, v, fb = oracle.c_rk4_chains(g["m"], g["C"], g["x0"], g["v0"], float(g["dt"]),
+                                           int(g["nsteps"]), int(g["stride"]))
+    assert not fb.any()
+    assert bits(xs) == bits(g["xs"]) and bits(vs) == bits(g["vs"])
+
+
 @pytest.mark.parametrize("where", ["wall", "free", "mid"])
 def test_c3_light_cone_windows(golden, where):
     g = golden(f"c3_window_{where}")

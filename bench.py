@@ -50,8 +50,10 @@ DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb1ELi256E", 2),
                   "C4": ("chain_rk4_kernelILi8ELb0ELb0E", 8)}
 
 
-def dp_inst_per_dof_step(config: str):
-    """(count, source) for the roofline_fp64 denominator."""
+def dp_inst_per_dof_step(config: str, div2_frac=None):
+    """(count, source) for the roofline_fp64 denominator.  K1 has two hot
+    loops (three- and two-operation division); div2_frac = the fraction of
+    systems running the two-operation one weights them."""
     if config not in DP_LOOP_KERNEL:
         return None, None
     try:
@@ -61,10 +63,16 @@ def dp_inst_per_dof_step(config: str):
         kern, dofs = DP_LOOP_KERNEL[config]
         from paper_1702_02207_b200 import _native
 
-        n = sass_stats.dp_per_iteration(_native.LIB_PATH, kern)
-        if n:
-            return n / dofs, (f"SASS of {kern}...: {n} DP instr per hot-loop iteration / "
-                              f"{dofs} DOF-steps")
+        loops = sass_stats.dp_loops(_native.LIB_PATH, kern)
+        if loops and div2_frac is not None and len(loops) >= 2:
+            n3, n2 = loops[0], loops[-1]
+            n = div2_frac * n2 + (1 - div2_frac) * n3
+            return n / dofs, (f"SASS of {kern}...: {n2} (two-operation division, "
+                              f"{div2_frac:.4f} of systems) / {n3} (three-operation) DP instr "
+                              f"per hot-loop iteration / {dofs} DOF-steps")
+        if loops:
+            return loops[0] / dofs, (f"SASS of {kern}...: {loops[0]} DP instr per hot-loop "
+                                     f"iteration / {dofs} DOF-steps")
     except Exception:  # noqa: BLE001 -- cuobjdump missing: fall back to the counted constant
         pass
     return DP_INST_PER_DOF_STEP[config], "constant (counted with scripts/sass_stats.py --loop)"
@@ -727,7 +735,12 @@ def main():
                     f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
                     f"is expected; its real limit is the FP64 pipe (roofline_fp64)",
         }
-    dp, dp_src = dp_inst_per_dof_step(wl.name)
+    div2_frac = None
+    if wl.name in ("C1", "C2") and os.environ.get("OSC_DIV2", "1")[:1] != "0":
+        # systems whose two masses admit the two-operation division
+        cls = wl.batched.div2_classify(wl.dev[0])
+        div2_frac = float((cls[0] & cls[1]).double().mean())
+    dp, dp_src = dp_inst_per_dof_step(wl.name, div2_frac)
     dp_inst_rate = per_gpu * dp if dp else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -755,7 +768,9 @@ def main():
         },
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (wl.launches + (3 if wl.name == "C5" else 0)) * args.steps,
+        # + C5: rowscale, pack, unpack; C1/C2: the division classifier and the
+        # two kernels of the launch-order partition (cub::DevicePartition)
+        "gpu_launches": (wl.launches + (3 if wl.name in ("C1", "C2", "C5") else 0)) * args.steps,
         "clocks": clocks.summary(),
         "step_ms": step_ms,
     }

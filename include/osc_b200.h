@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 8
+#define OSC_ABI_VERSION 9
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -218,9 +218,18 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
 
 /* Self-test of the hoisted-reciprocal division against IEEE div.rn.f64 on n
  * random operand pairs (mode 0: masses in [0.5,2), any numerator; 1: any
- * positive divisor; 2: physical ranges).  Synchronous; *mismatches (host)
- * receives the number of pairs whose bits differ. */
+ * positive divisor; 2: physical ranges; 3: the two-operation division of
+ * osc_rk4_batch2 on physical ranges; 4: the same on numerators next to
+ * quotient rounding midpoints).  Synchronous; *mismatches (host) receives the
+ * number of pairs whose bits differ. */
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream);
+
+/* pass[i] = 1 when b[i] admits the two-operation division q = RN(a*zh +
+ * RN(a*zl)) (zh = RN(1/b), zl = RN(1/b - zh)) for every numerator the
+ * kernels feed it: osc_rk4_batch2 runs the systems whose two masses pass
+ * with it (Brisebarre-Muller-Raina; osc_device.cuh).  Device buffers;
+ * enqueued on `stream`.  Not part of the reference interface (diagnostic). */
+int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream);
 
 /* FP64 pipe microbenchmark (roofline denominator; not part of the hot path):
  * enqueues one launch of 8 independent DFMA (mode 0) or DADD (mode 1)

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
-ABI_VERSION = 8
+ABI_VERSION = 9
 OSC_FMA = 1
 
 _i64 = ctypes.c_int64
@@ -62,6 +62,7 @@ SIGNATURES = {
     "osc_energy": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
     "osc_check_division": (ctypes.c_int, [_i64, ctypes.c_uint64, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_uint64), _vp]),
+    "osc_div2_classify": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
     "osc_bench_fp64": (ctypes.c_int, [_i64, ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int64),
                                        _vp]),
     "osc_rk4_batch2_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,

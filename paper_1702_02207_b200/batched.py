@@ -350,6 +350,17 @@ def check_division(n: int, seed: int = 1, mode: int = 0) -> int:
     return int(out.value)
 
 
+def div2_classify(b, *, stream=None) -> torch.Tensor:
+    """Bool tensor: which divisors admit the two-operation division that
+    osc_rk4_batch2 uses for systems whose two masses both pass."""
+    b = _dev(b)
+    out = torch.empty(b.numel(), dtype=torch.uint8, device=b.device)
+    rc = _native.lib().osc_div2_classify(_ptr(b), b.numel(), _ptr(out),
+                                         ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_div2_classify")
+    return out.bool().reshape(b.shape)
+
+
 # --------------------------------------------------------------------------
 # dense general (M, K) path (BASELINE configs[4]; K5)
 # --------------------------------------------------------------------------

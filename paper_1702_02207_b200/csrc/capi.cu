@@ -372,6 +372,14 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "energy_kernel");
 }
 
+int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream)
+{
+    if (n < 0 || (n > 0 && (!b || !pass)))
+        return fail(OSC_INVALID, "osc_div2_classify: n < 0 or null buffer");
+    cudaError_t e = osc::launch_div2_classify(b, n, pass, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "div2_classify_kernel");
+}
+
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream_)
 {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);

@@ -18,6 +18,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cub/device/device_partition.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 namespace osc {
 namespace {
 
@@ -108,6 +111,27 @@ __device__ __forceinline__ bool finite2(const Sys2 &s)
 
 constexpr int kChunk = 64;  // steps between divergence checks
 
+// Launch order of the systems for the two-operation division: cls[i] != 0
+// when both masses of system i pass div2_classify; order lists the passing
+// systems first (ascending), so all but one boundary warp are uniform.
+// order == nullptr: identity order, three-operation division everywhere.
+struct Div2Plan {
+    const int64_t *order;
+    const uint8_t *cls;
+};
+
+__global__ void batch2_classify_kernel(const double *__restrict__ m, int64_t B,
+                                       uint8_t *__restrict__ cls)
+{
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < B;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double zh, zl;
+        const bool a = div2_classify(m[i], zh, zl);
+        const bool b = div2_classify(m[B + i], zh, zl);
+        cls[i] = a && b;
+    }
+}
+
 // NS systems per thread, interleaved for instruction-level parallelism:
 // system j of thread t in block b is b*NS*blockDim + j*blockDim + t, so each
 // load/store of a warp stays one contiguous 256 B run.  Indices past B
@@ -120,27 +144,31 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
                   StepConsts k, int64_t nsteps, int64_t stride, double *__restrict__ xs,
                   double *__restrict__ vs, double *__restrict__ es,
-                  int64_t *__restrict__ first_bad, CmpArgs cmp = CmpArgs{})
+                  int64_t *__restrict__ first_bad, Div2Plan plan, CmpArgs cmp = CmpArgs{})
 {
     const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * NS + threadIdx.x;
     int64_t idx[NS];
     bool live[NS];
-    Divisor m0[NS], m1[NS];
+    // Divisor words of both masses: (b, y) for the three-operation division,
+    // (zh, zl) for the two-operation one.  A warp runs the two-operation
+    // division only when every one of its systems passed div2_classify
+    // (plan.order groups those systems); its exact replay re-reads b.
+    double u0[NS], w0[NS], u1[NS], w1[NS];
     double C0[NS], C1[NS];
     Sys2 s[NS];
     bool ok0 = true;
+    bool two = !kFma && plan.order != nullptr;
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
         const int64_t gi = base + static_cast<int64_t>(j) * blockDim.x;
         live[j] = gi < B;
-        idx[j] = live[j] ? gi : B - 1;
+        const int64_t g = live[j] ? gi : B - 1;
+        idx[j] = plan.order ? plan.order[g] : g;
         const int64_t i = idx[j];
-        m0[j] = make_divisor(m[i]);
-        m1[j] = make_divisor(m[B + i]);
+        two &= plan.order ? plan.cls[i] != 0 : false;
         C0[j] = C[i];
         C1[j] = C[B + i];
         s[j] = Sys2{x[i], x[B + i], v[i], v[B + i]};
-        ok0 &= divisor_fast_ok(m0[j]) & divisor_fast_ok(m1[j]);
         if (xs && live[j]) {
             xs[i] = s[j].x0;
             xs[B + i] = s[j].x1;
@@ -149,6 +177,19 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         }
         if (es && live[j])
             es[i] = energy2(s[j], m[i], m[B + i], C0[j], C1[j]);
+    }
+    two = __all_sync(kFull, two);
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        const int64_t i = idx[j];
+        if (two) {
+            div2_consts(m[i], u0[j], w0[j]);
+            div2_consts(m[B + i], u1[j], w1[j]);
+        } else {
+            const Divisor d0 = make_divisor(m[i]), d1 = make_divisor(m[B + i]);
+            u0[j] = d0.b, w0[j] = d0.y, u1[j] = d1.b, w1[j] = d1.y;
+            ok0 &= divisor_fast_ok(d0) & divisor_fast_ok(d1);
+        }
     }
     ErrAcc acc[kCmp ? NS : 1];
     if constexpr (kCmp) {
@@ -180,29 +221,47 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             // Throughput builds unroll 4 steps per iteration (loop control was
             // ~1% of the stall samples; +1.2% on C2).  The latency build (NS=1)
             // keeps one step per iteration: its schedule gets longer unrolled.
+            if (!kFma && two) {
 #pragma unroll(NS > 1 ? 4 : 1)
-            for (int t = 0; t < n; ++t) {
+                for (int t = 0; t < n; ++t) {
 #pragma unroll
-                for (int j = 0; j < NS; ++j)
-                    step2<kFma ? Arith::Fma : Arith::Fast>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
+                    for (int j = 0; j < NS; ++j)
+                        step2<Arith::Fast2>(s[j], C0[j], C1[j], Divisor{0.0, u0[j], w0[j]},
+                                            Divisor{0.0, u1[j], w1[j]}, k, ok);
+                }
+            } else {
+#pragma unroll(NS > 1 ? 4 : 1)
+                for (int t = 0; t < n; ++t) {
+#pragma unroll
+                    for (int j = 0; j < NS; ++j)
+                        step2<kFma ? Arith::Fma : Arith::Fast>(
+                            s[j], C0[j], C1[j], Divisor{u0[j], w0[j], 0.0},
+                            Divisor{u1[j], w1[j], 0.0}, k, ok);
+                }
             }
 #pragma unroll
             for (int j = 0; j < NS; ++j)
                 ok &= finite2(s[j]);
         }
         if (!ok) {
-            // A division left nvcc's fast path or a value went non-finite:
-            // replay the chunk with IEEE division, checking every step.
-            // Non-finite values are absorbing under + - * /, so the first
-            // non-finite step of each system is integrate's
+            // A division left the fast path's range or a value went
+            // non-finite: replay the chunk with IEEE division, checking every
+            // step.  Non-finite values are absorbing under + - * /, so the
+            // first non-finite step of each system is integrate's
             // NonFiniteStateError.step (oscillator.py:255-260).
 #pragma unroll
             for (int j = 0; j < NS; ++j)
                 s[j] = saved[j];
+            Divisor e0[NS], e1[NS];
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                e0[j] = Divisor{two ? m[idx[j]] : u0[j], w0[j], 0.0};
+                e1[j] = Divisor{two ? m[B + idx[j]] : u1[j], w1[j], 0.0};
+            }
             for (int t = 0; t < n; ++t) {
 #pragma unroll
                 for (int j = 0; j < NS; ++j) {
-                    step2<kFma ? Arith::Fma : Arith::Exact>(s[j], C0[j], C1[j], m0[j], m1[j], k, ok);
+                    step2<kFma ? Arith::Fma : Arith::Exact>(s[j], C0[j], C1[j], e0[j], e1[j], k, ok);
                     if (bad[j] == 0 && !finite2(s[j])) {
                         bad[j] = kstep + t + 1;
                         exact_only = true;
@@ -224,8 +283,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                         vs[o + B + i] = s[j].v1;
                     }
                     if (es)
-                        es[(kstep / stride) * B + i] =
-                            energy2(s[j], m0[j].b, m1[j].b, C0[j], C1[j]);
+                        es[(kstep / stride) * B + i] = energy2(s[j], m[i], m[B + i], C0[j], C1[j]);
                 }
             }
         }
@@ -270,7 +328,7 @@ template <int NS>
 cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, int64_t B,
                       StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
                       double *es, int64_t *first_bad, int threads, bool fma,
-                      cudaStream_t stream, const CmpArgs *cmp)
+                      cudaStream_t stream, const CmpArgs *cmp, Div2Plan plan)
 {
     const int64_t per_block = int64_t(threads) * NS;
     const unsigned blocks = static_cast<unsigned>((B + per_block - 1) / per_block);
@@ -280,22 +338,22 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
         // of the compare build (its compare switched off: null CmpArgs) ~4%
         // shorter than the others (profiles/r01/c1_latency.md).
         batch2_rk4_kernel<1, false, true><<<blocks, threads, 0, stream>>>(
-            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, CmpArgs{});
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, plan, CmpArgs{});
         return cudaGetLastError();
     }
     if (cmp) {
         if (fma)
             batch2_rk4_kernel<NS, true, true><<<blocks, threads, 0, stream>>>(
-                m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, *cmp);
+                m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, plan, *cmp);
         else
             batch2_rk4_kernel<NS, false, true><<<blocks, threads, 0, stream>>>(
-                m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, *cmp);
+                m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, plan, *cmp);
     } else if (fma)
         batch2_rk4_kernel<NS, true><<<blocks, threads, 0, stream>>>(
-            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, plan);
     else
         batch2_rk4_kernel<NS, false><<<blocks, threads, 0, stream>>>(
-            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad);
+            m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, plan);
     return cudaGetLastError();
 }
 
@@ -326,11 +384,54 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
             threads = b;
         }
     }
-    switch (ns) {
-    case 1: return launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp);
-    case 2: return launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp);
-    default: return launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp);
+    // Two-operation division (div2_classify): classify every system, then
+    // list the passing ones first.  OSC_DIV2=0 disables it (A/B timing); the
+    // FMA mode keeps its own x*(1/m).
+    Div2Plan plan{nullptr, nullptr};
+    void *scratch = nullptr;
+    const char *d2 = std::getenv("OSC_DIV2");
+    if (!fma && B > 0 && !(d2 && d2[0] == '0')) {
+        const thrust::counting_iterator<int64_t> ids(0);
+        size_t temp = 0;
+        cudaError_t e = cub::DevicePartition::Flagged(
+            nullptr, temp, ids, static_cast<const uint8_t *>(nullptr),
+            static_cast<int64_t *>(nullptr), static_cast<int64_t *>(nullptr), B, stream);
+        if (e != cudaSuccess)
+            return e;
+        const size_t off_cls = size_t(B + 1) * sizeof(int64_t);
+        const size_t off_tmp = (off_cls + size_t(B) + 255) & ~size_t(255);
+        if ((e = cudaMallocAsync(&scratch, off_tmp + temp, stream)) != cudaSuccess)
+            return e;
+        char *p = static_cast<char *>(scratch);
+        int64_t *order = reinterpret_cast<int64_t *>(p);
+        uint8_t *cls = reinterpret_cast<uint8_t *>(p + off_cls);
+        const int64_t want = (B + 255) / 256;
+        const unsigned grid = static_cast<unsigned>(want < int64_t(sms) * 8 ? want : int64_t(sms) * 8);
+        batch2_classify_kernel<<<grid, 256, 0, stream>>>(m, B, cls);
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cub::DevicePartition::Flagged(p + off_tmp, temp, ids, cls, order, order + B, B,
+                                              stream);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(scratch, stream);
+            return e;
+        }
+        plan = Div2Plan{order, cls};
     }
+    cudaError_t e;
+    switch (ns) {
+    case 1: e = launch_ns<1>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp, plan);
+        break;
+    case 2: e = launch_ns<2>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp, plan);
+        break;
+    default: e = launch_ns<4>(m, C, x, v, B, k, nsteps, stride, xs, vs, es, first_bad, threads, fma, stream, cmp, plan);
+    }
+    if (scratch) {
+        const cudaError_t f = cudaFreeAsync(scratch, stream);
+        if (e == cudaSuccess)
+            e = f;
+    }
+    return e;
 }
 
 }  // namespace osc

@@ -65,6 +65,9 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t z)
 //   mode 0: b in [0.5, 2) (the configs' masses), a any bit pattern
 //   mode 1: b any positive finite double (normal or subnormal), a any pattern
 //   mode 2: b in [0.5, 2), |a| in [2^-40, 2^40) (physical accelerations)
+//   mode 3: the two-operation division (div2_fast) as mode 2, divisors that
+//           pass div2_classify only
+//   mode 4: div2_fast on numerators next to quotient midpoints (see below)
 __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                                       unsigned long long *mismatches)
 {
@@ -86,11 +89,58 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
             bb = ((r2 >> 63) ? 0x3fe0000000000000ull : 0x3ff0000000000000ull) | mant_b;
         }
         uint64_t ab = r1;
-        if (mode == 2) {
+        if (mode == 2 || mode == 3) {
             const uint64_t e = 1023 - 40 + ((r1 >> 52) % 80);
             ab = (r1 & 0x800fffffffffffffull) | (e << 52);
         } else if ((r1 & 0xff) == 0) {
             ab = r1 & 0x8000000000000000ull;  // inject signed zeros
+        }
+        if (mode >= 3) {
+            // The two-operation division (div2_fast) on divisors that pass
+            // div2_classify; mode 4 aims every numerator at a rounding
+            // midpoint of the quotient: A 2^sh - B M = k for a random small
+            // k and binade (sh = 53: a/b >= 1, sh = 54: a/b < 1), and scales
+            // a and b by random powers of two inside the admissible ranges.
+            double b0 = __longlong_as_double(static_cast<long long>(bb));
+            if (mode == 4) {
+                const uint64_t B = mant_b | (1ull << 52);
+                const uint64_t Bo = B >> (__ffsll(static_cast<long long>(B)) - 1);
+                const int sh = (r1 & 1) ? 53 : 54;
+                const int ak = 1 + static_cast<int>((r1 >> 1) % 64);
+                const uint64_t lo = sh == 53 ? B : (1ull << 52), hi = sh == 53 ? (1ull << 53) : B;
+                uint64_t A = r1 >> 12 | (1ull << 52);  // a random significand when unsolvable
+                if (Bo == B && lo < hi) {
+                    A = (static_cast<uint64_t>(ak) * inv_pow2_mod(sh, B)) % B;
+                    if ((r1 >> 7) & 1)
+                        A = (B - A) % B;
+                    if (A < lo)
+                        A += ((lo - A + B - 1) / B) * B;
+                    if (A >= hi)
+                        A = r1 >> 12 | (1ull << 52);
+                }
+                const int ea = static_cast<int>((r1 >> 20) % 801) - 400;   // a in [2^-400, 2^401)
+                const int eb = static_cast<int>((r2 >> 53) % 181) - 90;    // b in [2^-90, 2^91)
+                ab = ((r1 >> 8) & 1ull) << 63 | (uint64_t(1023 + ea) << 52) |
+                     (A & 0x000fffffffffffffull);
+                b0 = __longlong_as_double(static_cast<long long>(
+                    (uint64_t(1023 + eb) << 52) | mant_b));
+            }
+            double zh, zl;
+            if (!div2_classify(b0, zh, zl))
+                continue;
+            double zh2, zl2;
+            div2_consts(b0, zh2, zl2);
+            const double a = __longlong_as_double(static_cast<long long>(ab));
+            bool ok = true;
+            const double got = div2_fast(a, Divisor{b0, zh2, zl2}, ok);
+            const double want = __ddiv_rn(a, b0);
+            // a counted pair: the range check passed and the bits differ, or
+            // the two constant computations disagree
+            if ((ok && __double_as_longlong(got) != __double_as_longlong(want)) ||
+                __double_as_longlong(zh) != __double_as_longlong(zh2) ||
+                __double_as_longlong(zl) != __double_as_longlong(zl2))
+                ++bad;
+            continue;
         }
         const double a = __longlong_as_double(static_cast<long long>(ab));
         const double b = __longlong_as_double(static_cast<long long>(bb));
@@ -290,6 +340,26 @@ cudaError_t launch_energy(const double *m, const double *C, const double *x, con
     const int threads = 128;
     energy_kernel<<<static_cast<unsigned>((B + threads - 1) / threads), threads, 0, stream>>>(
         m, C, x, v, out, B, s, cell_major ? 1 : s, cell_major ? B : 1);
+    return cudaGetLastError();
+}
+
+__global__ void div2_classify_kernel(const double *__restrict__ b, int64_t n,
+                                     uint8_t *__restrict__ pass)
+{
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double zh, zl;
+        pass[i] = div2_classify(b[i], zh, zl);
+    }
+}
+
+cudaError_t launch_div2_classify(const double *b, int64_t n, uint8_t *pass, cudaStream_t stream)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const int64_t want = (n + 255) / 256;
+    div2_classify_kernel<<<static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16), 256, 0,
+                           stream>>>(b, n, pass);
     return cudaGetLastError();
 }
 

@@ -68,6 +68,8 @@ cudaError_t launch_energy(const double *m, const double *C, const double *x, con
 cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *out,
                              cudaStream_t stream);
 
+cudaError_t launch_div2_classify(const double *b, int64_t n, uint8_t *pass, cudaStream_t stream);
+
 cudaError_t launch_check_division(int64_t n, uint64_t seed, int mode,
                                   unsigned long long *mismatches, cudaStream_t stream);
 

@@ -51,6 +51,28 @@ def loop_body(body):
     return best[1] if best else [i for _, i in body]
 
 
+def hot_loops(body):
+    """DP counts of the CALL-free loops holding at least half the DP
+    instructions of the largest one (K1 has two: three- and two-operation
+    division), largest first."""
+    out = []
+    for addr, ins in body:
+        m = re.search(r"\bBRA\b.*?0x([0-9a-f]+)\s*$", ins)
+        if m and int(m.group(1), 16) < addr:
+            seg = [i for a, i in body if int(m.group(1), 16) <= a <= addr]
+            if not any(opcode(i) == "CALL" for i in seg):
+                out.append(sum(opcode(i) in ("DADD", "DMUL", "DFMA") for i in seg))
+    out.sort(reverse=True)
+    return [n for n in out if out and n >= out[0] / 2]
+
+
+def dp_loops(lib, kernel_substr):
+    for name, body in functions(lib):
+        if kernel_substr in name:
+            return hot_loops(body)
+    return []
+
+
 def dp_per_iteration(lib, kernel_substr):
     """DP-pipe instructions in the hot loop of the first kernel whose mangled
     name contains kernel_substr (one loop iteration = one RK4 step)."""

@@ -1,0 +1,67 @@
+"""Exact-rational model of the two-operation division (test infrastructure).
+
+q = RN(a*zh + RN(a*zl)), zh = RN(1/b), zl = RN(1/b - zh) (Brisebarre,
+Muller, Raina 2004), restated with ``fractions.Fraction`` so every rounding is
+exact: Python's float(Fraction) and float ``*``/``/`` are correctly rounded.
+``classify`` mirrors div2_classify (paper_1702_02207_b200/csrc/osc_device.cuh):
+a divisor passes iff the two-operation quotient is correct on every
+significand A with A*2^sh = k (mod B), |k| <= 2 (sh = 53, a/b >= 1) and
+|k| <= 4 (sh = 54, a/b < 1).
+"""
+
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+
+def consts(b: float):
+    zh = 1.0 / b
+    zl = float(Fraction(1) / Fraction(b) - Fraction(zh))
+    return zh, zl
+
+
+def div2(a: float, zh: float, zl: float) -> float:
+    return float(Fraction(a) * Fraction(zh) + Fraction(a * zl))
+
+
+def significand(b: float):
+    m, e = math.frexp(b)  # b = m 2^e, m in [0.5, 1)
+    return int(m * 2 ** 53), e - 1
+
+
+def solutions(B: int, sh: int, k: int, lo: int, hi: int):
+    """Significands A in [lo, hi) with A 2^sh - B M = k for some integer M."""
+    g = math.gcd(B, 2 ** sh)
+    if k % g:
+        return []
+    Bo, kk = B // g, k // g
+    if Bo == 1:
+        return []
+    A = (kk * pow(2 ** sh // g, -1, Bo)) % Bo
+    if A < lo:
+        A += -(-(lo - A) // Bo) * Bo
+    return list(range(A, hi, Bo))
+
+
+def candidates(b: float, kmax53: int = 2, kmax54: int = 4):
+    B, _ = significand(b)
+    out = []
+    for sh, kmax, lo, hi in ((53, kmax53, B, 2 ** 53), (54, kmax54, 2 ** 52, B)):
+        for k in range(-kmax, kmax + 1):
+            if k:
+                out += [(sh, k, A) for A in solutions(B, sh, k, lo, hi)]
+    return out
+
+
+def classify(b: float) -> bool:
+    if not (2.0 ** -100 <= b < 2.0 ** 101):
+        return False
+    B, _ = significand(b)
+    bs = B / 2 ** 52
+    zh, zl = consts(bs)
+    if B == 2 ** 52:
+        return True
+    if abs(zl) < 2.0 ** -80 * zh:
+        return False
+    return all(div2(A / 2 ** 52, zh, zl) == (A / 2 ** 52) / bs for _, _, A in candidates(b))

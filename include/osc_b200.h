@@ -224,10 +224,13 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
  * number of pairs whose bits differ. */
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream);
 
-/* pass[i] = 1 when b[i] admits the two-operation division q = RN(a*zh +
- * RN(a*zl)) (zh = RN(1/b), zl = RN(1/b - zh)) for every numerator the
- * kernels feed it: osc_rk4_batch2 runs the systems whose two masses pass
- * with it (Brisebarre-Muller-Raina; osc_device.cuh).  Device buffers;
+/* pass[i] = the class of b[i] for the two-operation division q = RN(a*zh +
+ * RN(a*zl)) (zh = RN(1/b), zl = RN(1/b - zh); Brisebarre-Muller-Raina,
+ * osc_device.cuh): 1 = correctly rounded for every numerator the kernels
+ * feed it, 2 / 3 = the same with zl moved one ulp toward +inf / -inf, 0 =
+ * none.  osc_rk4_batch2 runs the systems whose two masses have a class with
+ * it (the chain kernels keep the three-operation division: DESIGN.md).
+ * Device buffers;
  * enqueued on `stream`.  Not part of the reference interface (diagnostic). */
 int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream);
 

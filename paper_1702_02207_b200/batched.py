@@ -351,14 +351,16 @@ def check_division(n: int, seed: int = 1, mode: int = 0) -> int:
 
 
 def div2_classify(b, *, stream=None) -> torch.Tensor:
-    """Bool tensor: which divisors admit the two-operation division that
-    osc_rk4_batch2 uses for systems whose two masses both pass."""
+    """uint8 tensor of divisor classes for the two-operation division
+    (osc_device.cuh div2_classify): 0 = none, 1-3 = admitted (zl itself, or
+    moved one ulp toward +inf / -inf).  osc_rk4_batch2 uses it for systems
+    whose two masses both have a class."""
     b = _dev(b)
     out = torch.empty(b.numel(), dtype=torch.uint8, device=b.device)
     rc = _native.lib().osc_div2_classify(_ptr(b), b.numel(), _ptr(out),
                                          ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_div2_classify")
-    return out.bool().reshape(b.shape)
+    return out.reshape(b.shape)
 
 
 # --------------------------------------------------------------------------

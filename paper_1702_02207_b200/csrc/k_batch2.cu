@@ -111,24 +111,27 @@ __device__ __forceinline__ bool finite2(const Sys2 &s)
 
 constexpr int kChunk = 64;  // steps between divergence checks
 
-// Launch order of the systems for the two-operation division: cls[i] != 0
-// when both masses of system i pass div2_classify; order lists the passing
-// systems first (ascending), so all but one boundary warp are uniform.
-// order == nullptr: identity order, three-operation division everywhere.
+// Launch order of the systems for the two-operation division: mcls [2][B]
+// holds the div2_classify class of every mass, sys[i] != 0 when both masses
+// of system i have one; order lists those systems first (ascending), so all
+// but one boundary warp are uniform.  order == nullptr: identity order,
+// three-operation division everywhere.
 struct Div2Plan {
     const int64_t *order;
-    const uint8_t *cls;
+    const uint8_t *mcls;
 };
 
 __global__ void batch2_classify_kernel(const double *__restrict__ m, int64_t B,
-                                       uint8_t *__restrict__ cls)
+                                       uint8_t *__restrict__ mcls, uint8_t *__restrict__ sys)
 {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < B;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double zh, zl;
-        const bool a = div2_classify(m[i], zh, zl);
-        const bool b = div2_classify(m[B + i], zh, zl);
-        cls[i] = a && b;
+        const int a = div2_classify(m[i], zh, zl);
+        const int b = div2_classify(m[B + i], zh, zl);
+        mcls[i] = static_cast<uint8_t>(a);
+        mcls[B + i] = static_cast<uint8_t>(b);
+        sys[i] = a != 0 && b != 0;
     }
 }
 
@@ -165,7 +168,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         const int64_t g = live[j] ? gi : B - 1;
         idx[j] = plan.order ? plan.order[g] : g;
         const int64_t i = idx[j];
-        two &= plan.order ? plan.cls[i] != 0 : false;
+        two &= plan.order ? (plan.mcls[i] != 0) & (plan.mcls[B + i] != 0) : false;
         C0[j] = C[i];
         C1[j] = C[B + i];
         s[j] = Sys2{x[i], x[B + i], v[i], v[B + i]};
@@ -183,8 +186,8 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
     for (int j = 0; j < NS; ++j) {
         const int64_t i = idx[j];
         if (two) {
-            div2_consts(m[i], u0[j], w0[j]);
-            div2_consts(m[B + i], u1[j], w1[j]);
+            div2_consts(m[i], plan.mcls[i], u0[j], w0[j]);
+            div2_consts(m[B + i], plan.mcls[B + i], u1[j], w1[j]);
         } else {
             const Divisor d0 = make_divisor(m[i]), d1 = make_divisor(m[B + i]);
             u0[j] = d0.b, w0[j] = d0.y, u1[j] = d1.b, w1[j] = d1.y;
@@ -398,25 +401,25 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
             static_cast<int64_t *>(nullptr), static_cast<int64_t *>(nullptr), B, stream);
         if (e != cudaSuccess)
             return e;
-        const size_t off_cls = size_t(B + 1) * sizeof(int64_t);
-        const size_t off_tmp = (off_cls + size_t(B) + 255) & ~size_t(255);
+        const size_t off_cls = size_t(B + 1) * sizeof(int64_t);  // mcls [2][B], sys [B]
+        const size_t off_tmp = (off_cls + 3 * size_t(B) + 255) & ~size_t(255);
         if ((e = cudaMallocAsync(&scratch, off_tmp + temp, stream)) != cudaSuccess)
             return e;
         char *p = static_cast<char *>(scratch);
         int64_t *order = reinterpret_cast<int64_t *>(p);
-        uint8_t *cls = reinterpret_cast<uint8_t *>(p + off_cls);
+        uint8_t *mcls = reinterpret_cast<uint8_t *>(p + off_cls), *sys = mcls + 2 * B;
         const int64_t want = (B + 255) / 256;
         const unsigned grid = static_cast<unsigned>(want < int64_t(sms) * 8 ? want : int64_t(sms) * 8);
-        batch2_classify_kernel<<<grid, 256, 0, stream>>>(m, B, cls);
+        batch2_classify_kernel<<<grid, 256, 0, stream>>>(m, B, mcls, sys);
         e = cudaGetLastError();
         if (e == cudaSuccess)
-            e = cub::DevicePartition::Flagged(p + off_tmp, temp, ids, cls, order, order + B, B,
+            e = cub::DevicePartition::Flagged(p + off_tmp, temp, ids, sys, order, order + B, B,
                                               stream);
         if (e != cudaSuccess) {
             cudaFreeAsync(scratch, stream);
             return e;
         }
-        plan = Div2Plan{order, cls};
+        plan = Div2Plan{order, mcls};
     }
     cudaError_t e;
     switch (ns) {

@@ -126,10 +126,11 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                     (uint64_t(1023 + eb) << 52) | mant_b));
             }
             double zh, zl;
-            if (!div2_classify(b0, zh, zl))
+            const int cls = div2_classify(b0, zh, zl);
+            if (!cls)
                 continue;
             double zh2, zl2;
-            div2_consts(b0, zh2, zl2);
+            div2_consts(b0, cls, zh2, zl2);
             const double a = __longlong_as_double(static_cast<long long>(ab));
             bool ok = true;
             const double got = div2_fast(a, Divisor{b0, zh2, zl2}, ok);
@@ -349,7 +350,7 @@ __global__ void div2_classify_kernel(const double *__restrict__ b, int64_t n,
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double zh, zl;
-        pass[i] = div2_classify(b[i], zh, zl);
+        pass[i] = static_cast<uint8_t>(div2_classify(b[i], zh, zl));
     }
 }
 

@@ -4,9 +4,10 @@ q = RN(a*zh + RN(a*zl)), zh = RN(1/b), zl = RN(1/b - zh) (Brisebarre,
 Muller, Raina 2004), restated with ``fractions.Fraction`` so every rounding is
 exact: Python's float(Fraction) and float ``*``/``/`` are correctly rounded.
 ``classify`` mirrors div2_classify (paper_1702_02207_b200/csrc/osc_device.cuh):
-a divisor passes iff the two-operation quotient is correct on every
-significand A with A*2^sh = k (mod B), |k| <= 2 (sh = 53, a/b >= 1) and
-|k| <= 4 (sh = 54, a/b < 1).
+class 1 (zl), 2 (zl one ulp toward +inf) or 3 (toward -inf) is the first
+whose two-operation quotient is correct on every significand A with
+A*2^sh = k (mod B), |k| <= 2 (sh = 53, a/b >= 1) and |k| <= 4 (sh = 54,
+a/b < 1); 0 = none.
 """
 
 from __future__ import annotations
@@ -54,14 +55,23 @@ def candidates(b: float, kmax53: int = 2, kmax54: int = 4):
     return out
 
 
-def classify(b: float) -> bool:
+def class_zl(zl: float, cls: int) -> float:
+    return zl if cls == 1 else math.nextafter(zl, math.inf if cls == 2 else -math.inf)
+
+
+def classify(b: float) -> int:
     if not (2.0 ** -100 <= b < 2.0 ** 101):
-        return False
+        return 0
     B, _ = significand(b)
     bs = B / 2 ** 52
     zh, zl = consts(bs)
     if B == 2 ** 52:
-        return True
-    if abs(zl) < 2.0 ** -80 * zh:
-        return False
-    return all(div2(A / 2 ** 52, zh, zl) == (A / 2 ** 52) / bs for _, _, A in candidates(b))
+        return 1
+    cands = candidates(b)
+    for cls in (1, 2, 3):
+        z = class_zl(zl, cls)
+        if abs(z) < 2.0 ** -80 * zh:
+            continue
+        if all(div2(A / 2 ** 52, zh, z) == (A / 2 ** 52) / bs for _, _, A in cands):
+            return cls
+    return 0

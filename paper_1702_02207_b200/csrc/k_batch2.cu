@@ -110,6 +110,10 @@ __device__ __forceinline__ bool finite2(const Sys2 &s)
 }
 
 constexpr int kChunk = 64;  // steps between divergence checks
+#ifndef OSC_B2_UNROLL
+#define OSC_B2_UNROLL 4  // steps per hot-loop iteration (variant builds: scripts/build_variants.py)
+#endif
+constexpr int kUnroll = OSC_B2_UNROLL;
 
 // Launch order of the systems for the two-operation division: mcls [2][B]
 // holds the div2_classify class of every mass, sys[i] != 0 when both masses
@@ -142,7 +146,7 @@ __global__ void batch2_classify_kernel(const double *__restrict__ m, int64_t B,
 // compare() against the analytic solution at every retained sample (when
 // cmp.sol is set).
 template <int NS, bool kFma, bool kCmp = false, int kMaxThreads = 256>
-__global__ void __launch_bounds__(kMaxThreads)
+__global__ void __launch_bounds__(kMaxThreads, (NS == 2 && kMaxThreads == 256) ? 2 : 1)
 batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ v, int64_t B,
                   StepConsts k, int64_t nsteps, int64_t stride, double *__restrict__ xs,
@@ -225,7 +229,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
             // ~1% of the stall samples; +1.2% on C2).  The latency build (NS=1)
             // keeps one step per iteration: its schedule gets longer unrolled.
             if (!kFma && two) {
-#pragma unroll(NS > 1 ? 4 : 1)
+#pragma unroll(NS > 1 ? kUnroll : 1)
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)
@@ -233,7 +237,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                                             Divisor{0.0, u1[j], w1[j]}, k, ok);
                 }
             } else {
-#pragma unroll(NS > 1 ? 4 : 1)
+#pragma unroll(NS > 1 ? kUnroll : 1)
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)

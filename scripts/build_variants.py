@@ -13,11 +13,16 @@ VARIANTS = {
     "rul8": ["-Xptxas", "--register-usage-level=8"],
     "rul10": ["-Xptxas", "--register-usage-level=10"],
     "O2": ["-Xptxas", "-O2"],
+    "u1": ["-DOSC_B2_UNROLL=1"],
+    "u2": ["-DOSC_B2_UNROLL=2"],
+    "u8": ["-DOSC_B2_UNROLL=8"],
 }
 
 if __name__ == "__main__":
     base = os.path.join(build.HERE, "_variants")
     for tag, flags in VARIANTS.items():
+        if len(sys.argv) > 1 and tag not in sys.argv[1:]:
+            continue
         d = os.path.join(base, tag)
         out = build.build(force=True, extra=flags, out=os.path.join(d, "libosc_b200.so"),
                           build_dir=os.path.join(d, "obj"))

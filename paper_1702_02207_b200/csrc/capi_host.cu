@@ -44,6 +44,11 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 21)}));
     if (!chains)
         nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 1024)));
+    if (const char *e = std::getenv("OSC_HOST_CHUNKS")) {  // benchmarking knob
+        const long long n = std::atoll(e);
+        if (!xs && n >= 1 && n <= 64)
+            nchunk = std::min<int64_t>(n, B);
+    }
     const int nstream = static_cast<int>(std::min<int64_t>(nchunk, 3));
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
     for (int i = 0; i < nstream; ++i)

@@ -53,6 +53,27 @@ def test_slow_path_operands_batch2():
     _check_batch2(m, C, x0, v0, 1e-4, 500, 100)
 
 
+def test_two_operation_division_range_edges():
+    """Masses at and around the two-operation division's admissible range
+    (2^-100 <= m < 2^101) and state magnitudes around its numerator range
+    (2^-500 <= |a| < 2^501): inside it the systems run the two-operation
+    loop, outside the three-operation one or the exact replay; every system
+    byte-equal to the oracle."""
+    rng = np.random.default_rng(5)
+    edges = np.array([2.0 ** -100, np.nextafter(2.0 ** -100, 0), 2.0 ** 101,
+                      np.nextafter(2.0 ** 101, 0), 2.0 ** -100 * 1.5, 2.0 ** 100 * 1.7, 1.0, 0.75])
+    B = 2048
+    m = rng.choice(edges, (2, B))
+    C = rng.uniform(500.0, 2000.0, (2, B)) * m  # keep omega^2 = C/m moderate
+    x0 = rng.standard_normal((2, B))
+    v0 = np.zeros((2, B))
+    scale = rng.choice([1.0, 2.0 ** -490, 2.0 ** -505, 2.0 ** 490, 2.0 ** 505], B)
+    x0 *= scale
+    cls = batched.div2_classify(m).cpu().numpy()
+    assert (cls == 0).any() and (cls != 0).any()
+    _check_batch2(m, C, x0, v0, 1e-4, 300, 100)
+
+
 def test_stride_not_dividing_nsteps():
     rng = np.random.default_rng(5)
     m, C = rng.uniform(0.5, 2, (2, 1000)), rng.uniform(500, 2000, (2, 1000))

@@ -62,7 +62,9 @@ int osc_abi_version(void);
 const char *osc_last_error(void);
 
 /* Process-wide side effect: entry points that need scratch memory
- * (osc_rk4_chains, osc_rk4_dense, the *_host forms) allocate it
+ * (osc_rk4_batch2 and its compare form -- the launch order of the
+ * two-operation division --, osc_rk4_chains, osc_rk4_dense, the *_host
+ * forms) allocate it
  * stream-ordered from the device's default memory pool and raise that pool's
  * release threshold once per device (cudaMemPoolAttrReleaseThreshold), so
  * repeated calls reuse the memory instead of re-mapping it. */

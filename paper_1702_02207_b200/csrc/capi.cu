@@ -25,6 +25,7 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
         return OSC_OK;
     if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
+    retain_pool_memory();
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs, es,
                                        first_bad, (flags & OSC_FMA) != 0,
                                        static_cast<cudaStream_t>(stream));
@@ -47,6 +48,7 @@ int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *
     if (!m || !C || !x || !v || !first_bad || !ts || !sol || !report)
         return fail(OSC_INVALID, "null buffer");
     const osc::CmpArgs cmp{ts, sol, report};
+    retain_pool_memory();
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, nullptr, nullptr,
                                        nullptr, first_bad, (flags & OSC_FMA) != 0,
                                        static_cast<cudaStream_t>(stream), &cmp);

@@ -5,7 +5,10 @@
 // read from HBM once and its final state written once, so the kernel is
 // bound by FP64 issue, not by the 48 B/DOF-step one-step-per-round-trip
 // roofline.  Layout is SoA [2][B]: coordinate 0 of every system,
-// then coordinate 1, so every load/store of a warp is one 256 B run.
+// then coordinate 1, so a warp's loads/stores are 256 B runs.  Divisions by
+// the masses take two operations (div2_fast, osc_device.cuh) in every warp
+// whose systems' masses all have a div2 class: a classify kernel and a
+// stable cub partition put those systems first (Div2Plan).
 //
 // acceleration_at for s = 2 (oscillator.py:160-164), with d1 = x1 - x0:
 //   i=0: left = x0 - 0.0 (== x0 exactly), a = (-C0)*x0, a += C1*d1, a /= m0
@@ -140,9 +143,11 @@ __global__ void batch2_classify_kernel(const double *__restrict__ m, int64_t B,
 }
 
 // NS systems per thread, interleaved for instruction-level parallelism:
-// system j of thread t in block b is b*NS*blockDim + j*blockDim + t, so each
-// load/store of a warp stays one contiguous 256 B run.  Indices past B
-// duplicate the last system and are never stored.  kCmp: also accumulate
+// slot j of thread t in block b is g = b*NS*blockDim + j*blockDim + t and
+// holds system order[g] (g itself without a plan).  The partition is stable,
+// so a warp's systems stay one contiguous 256 B run except where unclassed
+// systems were moved out; loads and stores happen once per run.  Slots past
+// B duplicate the last one and are never stored.  kCmp: also accumulate
 // compare() against the analytic solution at every retained sample (when
 // cmp.sol is set).
 template <int NS, bool kFma, bool kCmp = false, int kMaxThreads = 256>

@@ -222,7 +222,8 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
  * random operand pairs (mode 0: masses in [0.5,2), any numerator; 1: any
  * positive divisor; 2: physical ranges; 3: the two-operation division of
  * osc_rk4_batch2 on physical ranges; 4: the same on numerators next to
- * quotient rounding midpoints).  Synchronous; *mismatches (host) receives the
+ * quotient rounding midpoints; 5: the loops' three-operation division with
+ * its flag, any operands).  Synchronous; *mismatches (host) receives the
  * number of pairs whose bits differ. */
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream);
 

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             for (int j = 0; j < K; ++j) {
                 t.C[j] = sm[TILE + cl + j];
                 t.md[j] = make_divisor(sm[cl + j]);
-                ok &= divisor_fast_ok(t.md[j]);
+                ok &= kFma ? divisor_fast_ok(t.md[j]) : divisor_range_ok(t.md[j]);
             }
             t.Cn = (cl + K < TILE) ? sm[TILE + cl + K] : 1.0;
             double x[K], v[K];
@@ -418,8 +418,11 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 x[j] = sm[2 * TILE + cl + j];
                 v[j] = sm[3 * TILE + cl + j];
             }
+            // single-test division here (div_fastq): -5% instructions, C3
+            // +1.1%; the whole-chain kernel keeps div_fast, whose schedule
+            // ptxas handles better (profiles/r01/README.md)
             for (int64_t s = 0; s < g.nsteps; ++s)
-                step<K, false, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, edges, ok);
+                step<K, false, kFma ? Arith::Fma : Arith::FastQ>(t, x, v, g.k, edges, ok);
             if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                 // exact replay from the tile input still in shared memory
 #pragma unroll

@@ -68,6 +68,8 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t z)
 //   mode 3: the two-operation division (div2_fast) as mode 2, divisors that
 //           pass div2_classify only
 //   mode 4: div2_fast on numerators next to quotient midpoints (see below)
+//   mode 5: div_fastq with its flag (divisor_range_ok, quotient_fast_ok), b any
+//           positive double, a any pattern
 __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                                       unsigned long long *mismatches)
 {
@@ -78,7 +80,7 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
         const uint64_t r2 = splitmix(seed ^ (2 * static_cast<uint64_t>(i) + 1));
         const uint64_t mant_b = r2 & 0x000fffffffffffffull;
         uint64_t bb;
-        if (mode == 1) {
+        if (mode == 1 || (mode == 5 && ((r1 >> 11) & 1))) {
             uint64_t e = (r2 >> 52) & 0x7ff;
             if (e == 0x7ff)
                 e = 0x7fe;
@@ -94,6 +96,19 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
             ab = (r1 & 0x800fffffffffffffull) | (e << 52);
         } else if ((r1 & 0xff) == 0) {
             ab = r1 & 0x8000000000000000ull;  // inject signed zeros
+        }
+        if (mode == 5) {
+            // div_fastq (the tiled chain loop's division) with its flag:
+            // any numerator pattern, any positive divisor; a pair counts when
+            // both tests pass and the bits differ from div.rn.f64.
+            const double a = __longlong_as_double(static_cast<long long>(ab));
+            const double b = __longlong_as_double(static_cast<long long>(bb));
+            const Divisor d = make_divisor(b);
+            bool ok = divisor_range_ok(d);
+            const double got = div_fastq(a, d, ok);
+            if (ok && __double_as_longlong(got) != __double_as_longlong(__ddiv_rn(a, b)))
+                ++bad;
+            continue;
         }
         if (mode >= 3) {
             // The two-operation division (div2_fast) on divisors that pass

@@ -238,8 +238,9 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)
-                        step2<Arith::Fast2>(s[j], C0[j], C1[j], Divisor{0.0, u0[j], w0[j]},
-                                            Divisor{0.0, u1[j], w1[j]}, k, ok);
+                        step2<NS == 1 ? Arith::Fast2A : Arith::Fast2>(
+                            s[j], C0[j], C1[j], Divisor{0.0, u0[j], w0[j]},
+                            Divisor{0.0, u1[j], w1[j]}, k, ok);
                 }
             } else {
 #pragma unroll(NS > 1 ? kUnroll : 1)

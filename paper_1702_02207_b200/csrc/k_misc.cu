@@ -147,12 +147,13 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
             double zh2, zl2;
             div2_consts(b0, cls, zh2, zl2);
             const double a = __longlong_as_double(static_cast<long long>(ab));
-            bool ok = true;
+            bool ok = true, ok_a = true;
             const double got = div2_fast(a, Divisor{b0, zh2, zl2}, ok);
+            div2a_fast(a, Divisor{b0, zh2, zl2}, ok_a);  // same quotient, numerator test
             const double want = __ddiv_rn(a, b0);
-            // a counted pair: the range check passed and the bits differ, or
-            // the two constant computations disagree
-            if ((ok && __double_as_longlong(got) != __double_as_longlong(want)) ||
+            // a counted pair: either form's range test passed and the bits
+            // differ, or the two constant computations disagree
+            if (((ok || ok_a) && __double_as_longlong(got) != __double_as_longlong(want)) ||
                 __double_as_longlong(zh) != __double_as_longlong(zh2) ||
                 __double_as_longlong(zl) != __double_as_longlong(zl2))
                 ++bad;

@@ -733,13 +733,15 @@ def main():
             "algorithmic_bytes_per_launch": alg_bytes,
             "note": f"SURVEY 8d: 48 B per DOF-step (one step per HBM round trip); peak "
                     f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
-                    f"is expected; its real limit is the FP64 pipe (roofline_fp64)",
+                    f"is expected; its real limit is the FP64 pipe (roofline_fp64).  Launch "
+                    f"duration = device step time / launches_per_step (for C1/C2 it includes "
+                    f"the ~0.3 ms division classify + launch-order partition)",
         }
     div2_frac = None
     if wl.name in ("C1", "C2") and os.environ.get("OSC_DIV2", "1")[:1] != "0":
         # systems whose two masses admit the two-operation division
         cls = wl.batched.div2_classify(wl.dev[0])
-        div2_frac = float((cls[0] & cls[1]).double().mean())
+        div2_frac = float(((cls[0] != 0) & (cls[1] != 0)).double().mean())
     dp, dp_src = dp_inst_per_dof_step(wl.name, div2_frac)
     dp_inst_rate = per_gpu * dp if dp else None
     line = {

@@ -47,7 +47,7 @@ DP_INST_PER_DOF_STEP = {"C1": 42, "C2": 42, "C3": 47, "C4": 47, "C5": None}
 DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb1ELi256E", 2),
                   "C2": ("batch2_rk4_kernelILi2ELb0ELb0ELi256E", 16),
                   "C3": ("chain_tiles_persistentILi8ELi256ELb0E", 8),
-                  "C4": ("chain_rk4_kernelILi8ELb0ELb0E", 8)}
+                  "C4": ("chain_rk4_kernelILi8ELb0ELb0ELi128E", 8)}
 
 
 def dp_inst_per_dof_step(config: str, div2_frac=None):

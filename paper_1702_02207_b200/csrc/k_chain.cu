@@ -211,9 +211,14 @@ __device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v
 template <int K>
 constexpr int max_threads() { return K <= 1 ? 1024 : K <= 4 ? 512 : 256; }
 
-template <int K, bool kPad, bool kFma>
-__global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
+// kMaxT = 128 (K = 8 whole chains of <= 1024 cells, C4): two CTAs per SM
+// promised to ptxas, which then keeps the single-test division's loop free
+// of rematerialised indices; it divides with div_fastq (one FSETP per
+// division).  The wider builds keep div_fast (profiles/r01/README.md).
+template <int K, bool kPad, bool kFma, int kMaxT = max_threads<K>()>
+__global__ void __launch_bounds__(kMaxT, kMaxT == 128 ? 2 : 1) chain_rk4_kernel(SegArgs g)
 {
+    constexpr bool kQ = kMaxT == 128 && K == 8;
     __shared__ Edges edges;
     __shared__ int s_skip;
     const int64_t buf_id = blockIdx.x / g.tiles;
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
         const int64_t c = c0 + j;
         t.C[j] = c < cend ? g.C[base + c] : 1.0;
         t.md[j] = make_divisor(c < cend ? g.m[base + c] : 1.0);
-        ok0 &= divisor_fast_ok(t.md[j]);
+        ok0 &= (kQ && !kFma) ? divisor_range_ok(t.md[j]) : divisor_fast_ok(t.md[j]);
     }
     t.Cn = (c0 + K < cend) ? g.C[base + c0 + K] : 1.0;
 
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(max_threads<K>()) chain_rk4_kernel(SegArgs g)
     load_state<K>(g, base, c0, cend, x, v);
     bool ok = ok0;
     for (int64_t s = 0; s < g.nsteps; ++s)
-        step<K, kPad, kFma ? Arith::Fma : Arith::Fast>(t, x, v, g.k, edges, ok);
+        step<K, kPad, kFma ? Arith::Fma : (kQ ? Arith::FastQ : Arith::Fast)>(t, x, v, g.k, edges, ok);
 
     if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, own_start, own_end))) {
         // A division left nvcc's fast path, or a value went non-finite:
@@ -485,6 +490,15 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
     const int64_t TILE = int64_t(threads) * K;
     const unsigned nb = static_cast<unsigned>(blocks);
     // Padding is needed only when a tile is longer than the whole buffer.
+    if (K == 8 && threads <= 128) {
+        if (TILE > g.n)
+            (g.fma ? chain_rk4_kernel<K, true, true, 128> : chain_rk4_kernel<K, true, false, 128>)
+                <<<nb, threads, 0, stream>>>(g);
+        else
+            (g.fma ? chain_rk4_kernel<K, false, true, 128> : chain_rk4_kernel<K, false, false, 128>)
+                <<<nb, threads, 0, stream>>>(g);
+        return cudaGetLastError();
+    }
     if (TILE > g.n)
         (g.fma ? chain_rk4_kernel<K, true, true> : chain_rk4_kernel<K, true, false>)
             <<<nb, threads, 0, stream>>>(g);

@@ -41,7 +41,8 @@ def test_batch2_hot_loops(kernels):
 def test_chain_hot_loops(kernels):
     import sass_stats
 
-    for kern in ("chain_tiles_persistentILi8ELi256ELb0E", "chain_rk4_kernelILi8ELb0ELb0E"):
+    for kern in ("chain_tiles_persistentILi8ELi256ELb0E", "chain_rk4_kernelILi8ELb0ELb0ELi128E",
+                 "chain_rk4_kernelILi8ELb0ELb0ELi256E"):
         assert sass_stats.hot_loops(_body(kernels, kern))[0] == 47 * 8, kern
 
 
@@ -53,7 +54,7 @@ def test_no_local_memory_in_hot_loops(kernels):
     for name, body in kernels.items():
         if not any(k in name for k in ("batch2_rk4_kernelILi2ELb0ELb0ELi256E",
                                        "chain_tiles_persistentILi8ELi256ELb0E",
-                                       "chain_rk4_kernelILi8ELb0ELb0E")):
+                                       "chain_rk4_kernelILi8ELb0ELb0ELi128E")):
             continue
         for addr, ins in body:
             m = re.search(r"\bBRA\b.*?0x([0-9a-f]+)\s*$", ins)

@@ -211,14 +211,15 @@ __device__ __forceinline__ bool owned_bad(const double (&x)[K], const double (&v
 template <int K>
 constexpr int max_threads() { return K <= 1 ? 1024 : K <= 4 ? 512 : 256; }
 
-// kMaxT = 128 (K = 8 whole chains of <= 1024 cells, C4): two CTAs per SM
-// promised to ptxas, which then keeps the single-test division's loop free
-// of rematerialised indices; it divides with div_fastq (one FSETP per
-// division).  The wider builds keep div_fast (profiles/r01/README.md).
+// K * kMaxT = 1024 (K = 8 x 128 threads -- C4 -- or K = 4 x 256): two CTAs
+// per SM promised to ptxas, which then keeps the single-test division's
+// loop free of rematerialised indices; these builds divide with div_fastq
+// (one FSETP per division).  The wider builds keep div_fast
+// (profiles/r01/README.md).
 template <int K, bool kPad, bool kFma, int kMaxT = max_threads<K>()>
-__global__ void __launch_bounds__(kMaxT, kMaxT == 128 ? 2 : 1) chain_rk4_kernel(SegArgs g)
+__global__ void __launch_bounds__(kMaxT, K * kMaxT == 1024 ? 2 : 1) chain_rk4_kernel(SegArgs g)
 {
-    constexpr bool kQ = kMaxT == 128 && K == 8;
+    constexpr bool kQ = K * kMaxT == 1024 && K >= 4;
     __shared__ Edges edges;
     __shared__ int s_skip;
     const int64_t buf_id = blockIdx.x / g.tiles;
@@ -490,12 +491,13 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
     const int64_t TILE = int64_t(threads) * K;
     const unsigned nb = static_cast<unsigned>(blocks);
     // Padding is needed only when a tile is longer than the whole buffer.
-    if (K == 8 && threads <= 128) {
+    constexpr int kT2 = 1024 / K;  // two CTAs of <= 1024 cells per SM
+    if (K >= 4 && threads <= kT2) {
         if (TILE > g.n)
-            (g.fma ? chain_rk4_kernel<K, true, true, 128> : chain_rk4_kernel<K, true, false, 128>)
+            (g.fma ? chain_rk4_kernel<K, true, true, kT2> : chain_rk4_kernel<K, true, false, kT2>)
                 <<<nb, threads, 0, stream>>>(g);
         else
-            (g.fma ? chain_rk4_kernel<K, false, true, 128> : chain_rk4_kernel<K, false, false, 128>)
+            (g.fma ? chain_rk4_kernel<K, false, true, kT2> : chain_rk4_kernel<K, false, false, kT2>)
                 <<<nb, threads, 0, stream>>>(g);
         return cudaGetLastError();
     }

@@ -419,7 +419,7 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
         int64_t *order = reinterpret_cast<int64_t *>(p);
         uint8_t *mcls = reinterpret_cast<uint8_t *>(p + off_cls), *sys = mcls + 2 * B;
         const int64_t want = (B + 255) / 256;
-        const unsigned grid = static_cast<unsigned>(want < int64_t(sms) * 8 ? want : int64_t(sms) * 8);
+        const unsigned grid = static_cast<unsigned>(want < int64_t(sms) * 32 ? want : int64_t(sms) * 32);
         batch2_classify_kernel<<<grid, 256, 0, stream>>>(m, B, mcls, sys);
         e = cudaGetLastError();
         if (e == cudaSuccess)

@@ -217,7 +217,8 @@ constexpr int max_threads() { return K <= 1 ? 1024 : K <= 4 ? 512 : 256; }
 // (one FSETP per division).  The wider builds keep div_fast
 // (profiles/r01/README.md).
 template <int K, bool kPad, bool kFma, int kMaxT = max_threads<K>()>
-__global__ void __launch_bounds__(kMaxT, K * kMaxT == 1024 ? 2 : 1) chain_rk4_kernel(SegArgs g)
+__global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
+    chain_rk4_kernel(SegArgs g)
 {
     constexpr bool kQ = K * kMaxT == 1024 && K >= 4;
     __shared__ Edges edges;

@@ -51,10 +51,11 @@ def test_no_local_memory_in_hot_loops(kernels):
 
     import sass_stats
 
+    # every build of the time-step kernels (all shapes, FMA and compare
+    # variants): a launch bound that caps registers too low shows up here
     for name, body in kernels.items():
-        if not any(k in name for k in ("batch2_rk4_kernelILi2ELb0ELb0ELi256E",
-                                       "chain_tiles_persistentILi8ELi256ELb0E",
-                                       "chain_rk4_kernelILi8ELb0ELb0ELi128E")):
+        if not any(k in name for k in ("batch2_rk4_kernel", "chain_tiles_persistent",
+                                       "chain_rk4_kernel")):
             continue
         for addr, ins in body:
             m = re.search(r"\bBRA\b.*?0x([0-9a-f]+)\s*$", ins)
@@ -62,5 +63,5 @@ def test_no_local_memory_in_hot_loops(kernels):
                 seg = [i for a, i in body if int(m.group(1), 16) <= a <= addr]
                 ops = {sass_stats.opcode(i) for i in seg}
                 dp = sum(sass_stats.opcode(i) in ("DADD", "DMUL", "DFMA") for i in seg)
-                if dp > 300:
+                if dp >= 40 and "CALL" not in ops:
                     assert not ops & {"LDL", "STL"}, name

@@ -335,6 +335,28 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         : "memory");
 }
 
+// Bulk copy shared -> global (TMA engine, bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+
+// Neighbour ghost copies of an owned cell (the fused exchange of the peer
+// transport); the owned output itself leaves with the tile's bulk copy.
+__device__ __forceinline__ void store_peers(const SegArgs &g, int64_t c, double x, double v)
+{
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        const PeerGhost &p = g.peer[side];
+        if (p.x && c >= p.lo && c < p.hi) {
+            p.x[c + p.offset] = x;
+            p.v[c + p.offset] = v;
+        }
+    }
+}
+
 struct TileGeom {
     int64_t buf_id, base, L, own_start, own_end;
 };
@@ -446,15 +468,35 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                     }
                 }
             }
+            // The tile input is no longer needed: the results go into its x/v
+            // slots and leave as one bulk copy per array (TMA store) instead
+            // of 16 strided 8-byte stores per thread.
 #pragma unroll
             for (int j = 0; j < K; ++j) {
                 const int64_t c = c0 + j;
+                sm[2 * TILE + cl + j] = x[j];
+                sm[3 * TILE + cl + j] = v[j];
                 if (c >= tg.own_start && c < tg.own_end)
-                    store_owned(g, tg.base, c, x[j], v[j]);
+                    store_peers(g, c, x[j], v[j]);
             }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        __syncthreads();  // every thread is done with buffer b
+        __syncthreads();  // every thread is done with buffer b; the results are in it
         if (threadIdx.x == 0) {
+            if (!s_skip) {
+                const int64_t o = tg.own_start - tg.L;
+                const unsigned bytes = static_cast<unsigned>(tg.own_end - tg.own_start) * 8u;
+                const int64_t go = tg.base + tg.own_start;
+                bulk_s2g(g.xout + go, sm + 2 * TILE + o, bytes);
+                bulk_s2g(g.vout + go, sm + 3 * TILE + o, bytes);
+                if (g.xs) {
+                    bulk_s2g(g.xs + go, sm + 2 * TILE + o, bytes);
+                    bulk_s2g(g.vs + go, sm + 3 * TILE + o, bytes);
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the buffer is refilled below: its reads must be done
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
             const int64_t nx = it + 2 * int64_t(gridDim.x);
             if (nx < ntiles) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -462,6 +504,8 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             }
         }
     }
+    if (threadIdx.x == 0)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes performed
 }
 
 template <int K, int NT>
@@ -519,8 +563,8 @@ cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stre
     // kernel when the bulk copies are 16-byte aligned (even offsets).
     const int64_t TILE = int64_t(threads) * K;
     const bool tiled = g.H > 0 || g.tiles > 1;
-    const bool aligned = (g.n % 2 == 0) && (g.own_lo % 2 == 0) && (g.W % 2 == 0) &&
-                         (g.H % 2 == 0) && g.n >= TILE;
+    const bool aligned = (g.n % 2 == 0) && (g.own_lo % 2 == 0) && (g.own_hi % 2 == 0) &&
+                         (g.W % 2 == 0) && (g.H % 2 == 0) && g.n >= TILE;
     static const bool disable = std::getenv("OSC_NO_PERSIST") != nullptr;
     if (tiled && aligned && !disable) {
         if (K == 8 && threads == 128)

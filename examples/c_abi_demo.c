@@ -115,6 +115,21 @@ int main(int argc, char **argv)
         fprintf(stderr, "bad dt not rejected\n");
         return 1;
     }
+    {
+        /* the reference's parameter rule (oscillator.py:66-80): a zero mass is
+         * rejected before anything runs, the offender named, x untouched */
+        double m0 = m[B + 5], x5 = x[B + 5];
+        m[B + 5] = 0.0;
+        int which = -1;
+        int64_t idx = -1;
+        if (osc_rk4_batch2_host(m, C, x, v, B, 1e-4, 10, 10, NULL, NULL, fb) != OSC_INVALID ||
+            !osc_last_invalid_parameter(&which, &idx) || which != 0 || idx != B + 5 ||
+            x[B + 5] != x5) {
+            fprintf(stderr, "zero mass not rejected (%s)\n", osc_last_error());
+            return 1;
+        }
+        m[B + 5] = m0;
+    }
     double mm[2] = {0.002, 0.002}, cc[2] = {20250.0, 20250.0}, xx[2] = {2.0, -3.0},
            vv[2] = {0.0, 0.0};
     int64_t bad = 0;

@@ -50,16 +50,37 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 9
+#define OSC_ABI_VERSION 10
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
  * to the reference (measured tolerance in DESIGN.md / tests/test_gpu_fma.py).
  * 0 = the default, byte-identical arithmetic. */
 #define OSC_FMA 1u
+/* flags: OSC_TRUSTED -- the caller has already validated m and C (e.g. with
+ * osc_validate_parameters) and the entry point skips its own check.  Needed
+ * when the call is captured into a CUDA graph (the check synchronises the
+ * stream) and for per-period calls of a sharded run. */
+#define OSC_TRUSTED 2u
 
 int osc_abi_version(void);
 const char *osc_last_error(void);
+
+/* Parameter rule of the reference's OscillatorSystem (oscillator.py:66-80):
+ * every mass and spring rate must be positive and finite.  Every entry point
+ * that takes masses m and spring rates C (unless given OSC_TRUSTED) checks
+ * it on the device before integrating -- one pass over m and C, then a
+ * synchronisation of `stream`, so the call returns OSC_INVALID instead of
+ * enqueuing work -- and reports the first offender (masses before springs,
+ * lowest index first: the reference's order for one system).  After such an
+ * OSC_INVALID, osc_last_invalid_parameter returns 1 with which = 0 (masses)
+ * or 1 (springs) and *index = the flat element index into that array (for
+ * host entry points, into the caller's array); otherwise it returns 0.
+ * osc_validate_parameters runs the check alone over n device elements:
+ * OSC_OK, or OSC_INVALID with *bad (may be NULL) = the flat index. */
+int osc_validate_parameters(const double *m, const double *C, int64_t n, int64_t *bad,
+                            void *stream);
+int osc_last_invalid_parameter(int *which, int64_t *index);
 
 /* Process-wide side effect: entry points that need scratch memory
  * (osc_rk4_batch2 and its compare form -- the launch order of the
@@ -248,13 +269,25 @@ int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream);
 int osc_bench_fp64(int64_t iters, int mode, double *sink, int64_t *lane_ops, void *stream);
 
 /* Host-pointer convenience forms: synchronous, copies inside, return
- * OSC_NONFINITE when any system diverged. */
+ * OSC_NONFINITE when any system diverged.  The parameter rule is checked on
+ * the device before anything is written back: OSC_INVALID leaves x, v, xs,
+ * vs and first_bad untouched.  Small calls (<= 8 MB of data) are one round
+ * trip -- one host-to-device and one device-to-host copy through a pinned
+ * per-thread staging buffer, streams reused per thread -- which is the
+ * latency a drop-in caller stepping one small system sees; large ones are a
+ * chunked three-stream pipeline. */
 int osc_rk4_batch2_host(const double *m, const double *C, double *x, double *v, int64_t B,
                         double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
                         int64_t *first_bad);
 int osc_rk4_chains_host(const double *m, const double *C, double *x, double *v, int64_t B,
                         int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs,
                         double *vs, int64_t *first_bad);
+/* derivative() / energy() of host arrays (layouts as osc_derivative /
+ * osc_energy), one staged round trip each. */
+int osc_derivative_host(const double *m, const double *C, const double *x, double *dvel,
+                        int64_t B, int64_t s, int cell_major);
+int osc_energy_host(const double *m, const double *C, const double *x, const double *v,
+                    double *out, int64_t B, int64_t s, int cell_major);
 
 #ifdef __cplusplus
 }

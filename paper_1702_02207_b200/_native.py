@@ -16,8 +16,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
-ABI_VERSION = 9
+ABI_VERSION = 10
 OSC_FMA = 1
+OSC_TRUSTED = 2
 
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p
@@ -27,6 +28,10 @@ _dbl = ctypes.c_double
 SIGNATURES = {
     "osc_abi_version": (ctypes.c_int, []),
     "osc_last_error": (ctypes.c_char_p, []),
+    "osc_validate_parameters": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(ctypes.c_int64),
+                                               _vp]),
+    "osc_last_invalid_parameter": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int),
+                                                  ctypes.POINTER(ctypes.c_int64)]),
     "osc_rk4_batch2": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp, _vp,
                                       _vp, _vp, ctypes.c_uint32, _vp]),
     "osc_analytic_batch2": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
@@ -69,6 +74,8 @@ SIGNATURES = {
                                            _vp, _vp]),
     "osc_rk4_chains_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64,
                                            _vp, _vp, _vp]),
+    "osc_derivative_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int]),
+    "osc_energy_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int]),
 }
 
 
@@ -117,3 +124,12 @@ def lib() -> ctypes.CDLL:
 
 def last_error() -> str:
     return (load().osc_last_error() or b"").decode(errors="replace")
+
+
+def last_invalid_parameter():
+    """(which, flat index) of the offending parameter of this thread's last
+    OSC_INVALID -- which = 0 masses, 1 springs -- or None."""
+    which, index = ctypes.c_int(-1), ctypes.c_int64(-1)
+    if load().osc_last_invalid_parameter(ctypes.byref(which), ctypes.byref(index)):
+        return which.value, index.value
+    return None

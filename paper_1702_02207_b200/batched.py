@@ -54,12 +54,25 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def raise_for(rc: int, what: str):
-    """Map an OSC_* status to the reference's exception types."""
+def raise_for(rc: int, what: str, params=None):
+    """Map an OSC_* status to the reference's exception types.  A violated
+    parameter rule (the ABI's own check, osc_last_invalid_parameter) becomes
+    NonPositiveParameterError naming the element of ``params = (m, C)``."""
     if rc == _native.OSC_OK:
         return
     msg = f"{what}: {_native.last_error()}"
     if rc == _native.OSC_INVALID:
+        bad = _native.last_invalid_parameter()
+        if bad is not None:
+            which, index = bad
+            label = ("masses", "springs")[which]
+            if params is not None:
+                arr = params[which]
+                idx = tuple(int(i) for i in np.unravel_index(index, tuple(arr.shape)))
+                value = float(arr[idx])
+                raise NonPositiveParameterError(
+                    f"{label}{list(idx)} = {value!r}; must be positive and finite")
+            raise NonPositiveParameterError(msg)
         raise ValueError(msg)
     if rc == _native.OSC_NONFINITE:
         raise NonFiniteStateError(msg)
@@ -128,12 +141,11 @@ def analytic_batch2(m, C, x0, v0, *, stream=None) -> torch.Tensor:
     m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
     if m.dim() != 2 or m.shape[0] != 2 or not (m.shape == C.shape == x0.shape == v0.shape):
         raise ValueError(f"expected [2][B] arrays, got {tuple(m.shape)}")
-    validate_parameters(m, C)
     B = m.shape[1]
     sol = torch.empty((len(MODAL_FIELDS), B), dtype=torch.float64, device=m.device)
     rc = lib.osc_analytic_batch2(_ptr(m), _ptr(C), _ptr(x0), _ptr(v0), B, _ptr(sol),
                                  ctypes.c_void_p(_stream(stream)))
-    raise_for(rc, "osc_analytic_batch2")
+    raise_for(rc, "osc_analytic_batch2", (m, C))
     return sol
 
 
@@ -169,15 +181,20 @@ def _outputs(x0, v0, nsteps, stride, sample):
     return x, v, xs, vs
 
 
-def validate_parameters(m, C):
+def validate_parameters(m, C, *, stream=None):
     """OscillatorSystem's rule (oscillator.py:75-80) for whole batches: every
-    mass and spring rate positive and finite.  One device reduction."""
-    for label, a in (("masses", m), ("springs", C)):
-        bad = ~(torch.isfinite(a) & (a > 0))
-        if bool(bad.any()):
-            idx = tuple(int(i) for i in torch.nonzero(bad)[0])
-            raise NonPositiveParameterError(
-                f"{label}{list(idx)} = {float(a[idx])!r}; must be positive and finite")
+    mass and spring rate positive and finite -- the C ABI's own check
+    (osc_validate_parameters: one device pass), raising
+    NonPositiveParameterError for the first offender (masses first).  The
+    integrate entry points run the same check themselves; callers that
+    validated once pass ``validate=False`` (OSC_TRUSTED) afterwards."""
+    m, C = _dev(m), _dev(C)
+    if m.shape != C.shape:
+        raise ValueError(f"masses {tuple(m.shape)} vs springs {tuple(C.shape)}")
+    bad = ctypes.c_int64(-1)
+    rc = _native.lib().osc_validate_parameters(_ptr(m), _ptr(C), m.numel(), ctypes.byref(bad),
+                                               ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_validate_parameters", (m, C))
 
 
 def _energies(nsteps, stride, B, device, want):
@@ -202,15 +219,16 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
     m, C, x0, v0 = (_dev(a) for a in (m, C, x0, v0))
     if m.dim() != 2 or m.shape[0] != 2 or not (m.shape == C.shape == x0.shape == v0.shape):
         raise ValueError(f"expected [2][B] arrays, got {tuple(m.shape)}")
-    if validate:
-        validate_parameters(m, C)
     B = m.shape[1]
-    flags = _native.OSC_FMA if fma else 0
+    flags = (_native.OSC_FMA if fma else 0) | (0 if validate else _native.OSC_TRUSTED)
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
     errors = None
     if compare:
-        sol = _dev(analytic) if analytic is not None else analytic_batch2(m, C, x0, v0,
-                                                                         stream=stream)
+        if analytic is None:  # osc_analytic_batch2 applies the parameter rule itself
+            sol = analytic_batch2(m, C, x0, v0, stream=stream)
+            flags |= _native.OSC_TRUSTED
+        else:
+            sol = _dev(analytic)
         ts = _dev(accumulated_times(float(t0), float(dt), int(nsteps), int(stride)))
     if compare and not (sample or energies):
         x, v = x0.clone(), v0.clone()
@@ -219,7 +237,7 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
         rc = lib.osc_rk4_batch2_compare(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt),
                                         int(nsteps), int(stride), _ptr(ts), _ptr(sol), _ptr(out),
                                         _ptr(fb), flags, ctypes.c_void_p(_stream(stream)))
-        raise_for(rc, "osc_rk4_batch2_compare")
+        raise_for(rc, "osc_rk4_batch2_compare", (m, C))
         errors = _reports(out)
     else:
         x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample or compare)
@@ -227,7 +245,7 @@ def integrate_batch2(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
         rc = lib.osc_rk4_batch2(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, float(dt), int(nsteps),
                                 int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb), flags,
                                 ctypes.c_void_p(_stream(stream)))
-        raise_for(rc, "osc_rk4_batch2")
+        raise_for(rc, "osc_rk4_batch2", (m, C))
         if compare:
             errors = compare_batch2(sol, xs, ts, stream=stream)
             bad = fb > 0
@@ -250,17 +268,16 @@ def integrate_chains(m, C, x0, v0, dt, nsteps, stride=None, *, sample=False, ene
         m, C, x0, v0 = (a[None] for a in (m, C, x0, v0))
     if not (m.shape == C.shape == x0.shape == v0.shape) or m.dim() != 2:
         raise ValueError(f"expected [B][s] arrays, got {tuple(m.shape)}")
-    if validate:
-        validate_parameters(m, C)
     B, s = m.shape
     x, v, xs, vs = _outputs(x0, v0, nsteps, stride, sample)
     es = _energies(nsteps, stride, B, m.device, energies)
     fb = torch.zeros(B, dtype=torch.int64, device=m.device)
     rc = lib.osc_rk4_chains(_ptr(m), _ptr(C), _ptr(x), _ptr(v), B, s, float(dt), int(nsteps),
                             int(stride), _ptr(xs), _ptr(vs), _ptr(es), _ptr(fb),
-                            int(halo_steps), _native.OSC_FMA if fma else 0,
+                            int(halo_steps),
+                            (_native.OSC_FMA if fma else 0) | (0 if validate else _native.OSC_TRUSTED),
                             ctypes.c_void_p(_stream(stream)))
-    raise_for(rc, "osc_rk4_chains")
+    raise_for(rc, "osc_rk4_chains", (m, C))
     res = BatchResult(x, v, xs, vs, fb, float(dt), int(nsteps), int(stride), float(t0),
                       energies=es)
     return res.check() if check else res
@@ -276,7 +293,6 @@ def integrate_chain_sharded(m, C, x0, v0, dt, nsteps, devices, *, halo_steps=0, 
     x, v = (np.array(a, np.float64, order="C") for a in (x0, v0))
     if not (m.shape == C.shape == x.shape == v.shape) or m.ndim != 1:
         raise ValueError("expected four [s] arrays")
-    validate_parameters(torch.from_numpy(m), torch.from_numpy(C))
     devs = (ctypes.c_int * len(devices))(*devices)
     fb = np.zeros(1, np.int64)
     rc = lib.osc_rk4_chain_sharded(len(devices), devs, m.ctypes.data, C.ctypes.data,
@@ -286,7 +302,7 @@ def integrate_chain_sharded(m, C, x0, v0, dt, nsteps, devices, *, halo_steps=0, 
     if rc == _native.OSC_NONFINITE:
         raise NonFiniteStateError(f"integration diverged at step {int(fb[0])}",
                                   step=int(fb[0]))
-    raise_for(rc, "osc_rk4_chain_sharded")
+    raise_for(rc, "osc_rk4_chain_sharded", (m, C))
     return x, v
 
 
@@ -301,7 +317,7 @@ def chain_plan(B, s, nsteps, halo_steps=0) -> dict:
 
 
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None, fma=False, left=None, right=None):
+                  stream=None, fma=False, left=None, right=None, trusted=False):
     """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance).
 
     ``left``/``right``: optional ``(x, v, offset, count)`` -- a neighbour's
@@ -313,8 +329,9 @@ def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
     rc = _native.lib().osc_rk4_chain_advance(
         _ptr(m), _ptr(C), _ptr(xin), _ptr(vin), _ptr(xout), _ptr(vout), m.numel(), int(own_lo),
         int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad), peers[0], peers[1],
-        _native.OSC_FMA if fma else 0, ctypes.c_void_p(_stream(stream)))
-    raise_for(rc, "osc_rk4_chain_advance")
+        (_native.OSC_FMA if fma else 0) | (_native.OSC_TRUSTED if trusted else 0),
+        ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_rk4_chain_advance", (m, C))
 
 
 def derivative_chains(m, C, x, *, cell_major=False, stream=None) -> torch.Tensor:
@@ -325,7 +342,7 @@ def derivative_chains(m, C, x, *, cell_major=False, stream=None) -> torch.Tensor
     out = torch.empty_like(x)
     rc = lib.osc_derivative(_ptr(m), _ptr(C), _ptr(x), _ptr(out), B, s,
                                       int(cell_major), ctypes.c_void_p(_stream(stream)))
-    raise_for(rc, "osc_derivative")
+    raise_for(rc, "osc_derivative", (m, C))
     return out
 
 
@@ -337,7 +354,7 @@ def energy_chains(m, C, x, v, *, cell_major=False, stream=None) -> torch.Tensor:
     out = torch.empty(B, dtype=torch.float64, device=x.device)
     rc = lib.osc_energy(_ptr(m), _ptr(C), _ptr(x), _ptr(v), _ptr(out), B, s,
                                   int(cell_major), ctypes.c_void_p(_stream(stream)))
-    raise_for(rc, "osc_energy")
+    raise_for(rc, "osc_energy", (m, C))
     return out
 
 
@@ -376,7 +393,7 @@ def rowscale(K, m, *, stream=None) -> torch.Tensor:
         raise ValueError(f"K must be [{s}][{s}], got {tuple(K.shape)}")
     A = torch.empty_like(K)
     raise_for(lib.osc_rowscale(_ptr(K), _ptr(m), _ptr(A), s, ctypes.c_void_p(_stream(stream))),
-              "osc_rowscale")
+              "osc_rowscale", (m, m))
     return A
 
 

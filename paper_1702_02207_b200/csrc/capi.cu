@@ -15,7 +15,7 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
                    int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
                    int64_t *first_bad, uint32_t flags, void *stream)
 {
-    if (flags & ~uint32_t(OSC_FMA))
+    if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, stride))
         return rc;
@@ -25,6 +25,10 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
         return OSC_OK;
     if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
+    if (!(flags & OSC_TRUSTED))
+        if (int rc = check_params(m, C, 2 * B, static_cast<cudaStream_t>(stream),
+                                  ParamLayout::CellMajor, B))
+            return rc;
     retain_pool_memory();
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs, es,
                                        first_bad, (flags & OSC_FMA) != 0,
@@ -37,7 +41,7 @@ int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *
                            const double *sol, double *report, int64_t *first_bad, uint32_t flags,
                            void *stream)
 {
-    if (flags & ~uint32_t(OSC_FMA))
+    if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, stride))
         return rc;
@@ -47,6 +51,10 @@ int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *
         return OSC_OK;
     if (!m || !C || !x || !v || !first_bad || !ts || !sol || !report)
         return fail(OSC_INVALID, "null buffer");
+    if (!(flags & OSC_TRUSTED))
+        if (int rc = check_params(m, C, 2 * B, static_cast<cudaStream_t>(stream),
+                                  ParamLayout::CellMajor, B))
+            return rc;
     const osc::CmpArgs cmp{ts, sol, report};
     retain_pool_memory();
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, nullptr, nullptr,
@@ -64,6 +72,9 @@ int osc_analytic_batch2(const double *m, const double *C, const double *x0, cons
         return OSC_OK;
     if (!m || !C || !x0 || !v0 || !sol)
         return fail(OSC_INVALID, "null buffer");
+    if (int rc = check_params(m, C, 2 * B, static_cast<cudaStream_t>(stream),
+                              ParamLayout::CellMajor, B))
+        return rc;
     cudaError_t e = osc::launch_modal_batch2(m, C, x0, v0, B, sol,
                                              static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "modal_batch2_kernel");
@@ -89,7 +100,7 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
                    double dt, int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
                    int64_t *first_bad, int64_t halo_steps, uint32_t flags, void *stream_)
 {
-    if (flags & ~uint32_t(OSC_FMA))
+    if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, stride))
         return rc;
@@ -103,6 +114,9 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     const int64_t cells = B * s;
     const size_t bytes = sizeof(double) * static_cast<size_t>(cells);
+    if (!(flags & OSC_TRUSTED))
+        if (int rc = check_params(m, C, cells, stream, ParamLayout::Chains, B, s))
+            return rc;
 
     osc::SegArgs g{};
     g.m = m;
@@ -238,7 +252,7 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
                           const osc_peer_t *left, const osc_peer_t *right, uint32_t flags,
                           void *stream)
 {
-    if (flags & ~uint32_t(OSC_FMA))
+    if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, 1))
         return rc;
@@ -247,6 +261,9 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
                     (long long)own_hi, (long long)n);
     if (!m || !C || !xin || !vin || !xout || !vout || !first_bad)
         return fail(OSC_INVALID, "null buffer");
+    if (!(flags & OSC_TRUSTED))
+        if (int rc = check_params(m, C, n, static_cast<cudaStream_t>(stream)))
+            return rc;
     osc::SegArgs g{};
     g.m = m;
     g.C = C;
@@ -288,6 +305,8 @@ int osc_rowscale(const double *K, const double *m, double *A, int64_t s, void *s
 {
     if (s < 1 || !K || !m || !A)
         return fail(OSC_INVALID, "bad rowscale arguments");
+    if (int rc = check_params(m, m, s, static_cast<cudaStream_t>(stream)))  // masses only
+        return rc;
     cudaError_t e = osc::launch_rowscale(K, m, A, s, s, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "rowscale_kernel");
 }
@@ -348,6 +367,8 @@ int osc_equation_engine(const double *m, const double *C, const double *x0, cons
                     (long long)s);
     if (!m || !C || !x0 || !v0 || !first_bad || !step_ns || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
+    if (int rc = check_params(m, C, s, static_cast<cudaStream_t>(stream)))
+        return rc;
     cudaError_t e = osc::launch_equation_engine(m, C, x0, v0, static_cast<int>(s), dt, nsteps,
                                                 stride, xs, vs, first_bad, step_ns,
                                                 static_cast<cudaStream_t>(stream));
@@ -359,6 +380,13 @@ int osc_derivative(const double *m, const double *C, const double *x, double *dv
 {
     if (B < 0 || s < 1)
         return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x)
+        return fail(OSC_INVALID, "null buffer");
+    if (int rc = check_params(m, C, B * s, static_cast<cudaStream_t>(stream),
+                              cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s))
+        return rc;
     cudaError_t e = osc::launch_derivative(m, C, x, dvel, B, s, cell_major != 0,
                                            static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "derivative_kernel");
@@ -369,9 +397,40 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
 {
     if (B < 0 || s < 1)
         return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x)
+        return fail(OSC_INVALID, "null buffer");
+    if (int rc = check_params(m, C, B * s, static_cast<cudaStream_t>(stream),
+                              cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s))
+        return rc;
     cudaError_t e = osc::launch_energy(m, C, x, v, out, B, s, cell_major != 0,
                                        static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "energy_kernel");
+}
+
+int osc_validate_parameters(const double *m, const double *C, int64_t n, int64_t *bad,
+                            void *stream)
+{
+    if (bad)
+        *bad = -1;
+    if (n < 0 || (n > 0 && (!m || !C)))
+        return fail(OSC_INVALID, "osc_validate_parameters: n < 0 or null buffer");
+    const int rc = check_params(m, C, n, static_cast<cudaStream_t>(stream));
+    if (rc == OSC_INVALID && bad && g_bad_param_which >= 0)
+        *bad = g_bad_param_index;
+    return rc;
+}
+
+int osc_last_invalid_parameter(int *which, int64_t *index)
+{
+    if (g_bad_param_which < 0)
+        return 0;
+    if (which)
+        *which = g_bad_param_which;
+    if (index)
+        *index = g_bad_param_index;
+    return 1;
 }
 
 int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream)

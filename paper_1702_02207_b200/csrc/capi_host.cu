@@ -5,8 +5,6 @@
 
 using namespace osc_capi;
 
-extern "C" {
-
 // ---------------------------------------------------------------------------
 // Host-pointer forms: the end-to-end path a CPU caller (the reference's own
 // Python objects via ctypes) uses.  One cudaMemcpyAsync per buffer.
@@ -14,11 +12,132 @@ extern "C" {
 
 namespace {
 
-// Host-pointer form of a batched run.  The batch is cut into chunks that are
-// pipelined over a few streams: chunk c's H2D copy, kernels and D2H copy are
-// ordered on stream c % S, so copies of one chunk overlap the compute of
-// another and consecutive chunks' kernels fill each other's tail waves.
-// Sampled runs use a single chunk (their [nsamp][...] layout spans the batch).
+// Per-thread, per-device resources of the host-pointer forms, created once
+// and reused: the pipeline's streams (creating and destroying three streams
+// cost more than a small run itself) and a pinned staging buffer through
+// which small calls move all their inputs in ONE host-to-device copy and
+// all their outputs in ONE device-to-host copy.
+struct HostCtx {
+    int dev = -1;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+    unsigned char *pin = nullptr;
+    size_t pin_cap = 0;
+
+    ~HostCtx()
+    {
+        // thread exit; errors (runtime already unloading) are ignored
+        if (dev < 0)
+            return;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+        for (auto s : st)
+            if (s)
+                cudaStreamDestroy(s);
+        if (pin)
+            cudaFreeHost(pin);
+        cudaSetDevice(prev);
+        cudaGetLastError();
+    }
+};
+
+constexpr size_t kStagedMax = size_t(8) << 20;  // calls moving <= 8 MB go through staging
+
+int host_ctx(HostCtx *&out)
+{
+    static thread_local std::vector<HostCtx> ctx;
+    int dev = 0;
+    OSC_CUDA(cudaGetDevice(&dev));
+    if (ctx.size() <= static_cast<size_t>(dev))
+        ctx.resize(dev + 1);
+    HostCtx &c = ctx[dev];
+    if (c.dev < 0) {
+        for (auto &s : c.st)
+            OSC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        c.dev = dev;
+    }
+    out = &c;
+    return OSC_OK;
+}
+
+int staging(HostCtx &c, size_t bytes, unsigned char *&p)
+{
+    if (c.pin_cap < bytes) {
+        if (c.pin)
+            OSC_CUDA(cudaFreeHost(c.pin));
+        c.pin = nullptr;
+        c.pin_cap = 0;
+        const size_t cap = std::max<size_t>(bytes, size_t(1) << 16);
+        OSC_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&c.pin), cap, cudaHostAllocDefault));
+        c.pin_cap = cap;
+    }
+    p = c.pin;
+    return OSC_OK;
+}
+
+// A small host-pointer call, as one round trip through the pinned staging
+// buffer: the inputs go up in one copy, the parameter rule is checked ON
+// THE DEVICE in the same stream as the work (no extra synchronisation), the
+// outputs and the check result come back in one copy, and only then is
+// anything written to the caller's buffers -- an invalid system returns
+// OSC_INVALID with the caller's outputs untouched.
+//
+// Layout (device block and staging alike, all 8-byte slots):
+//   [ inputs (in_slots) | outputs (out_slots) | badp[2] ]
+// `work` enqueues the computation given the device block; `check` names the
+// parameter arrays to validate (slot offsets into the block, n elements).
+template <class Work>
+int staged_call(size_t in_slots, size_t out_slots, size_t m_off, size_t C_off, int64_t nparam,
+                const std::vector<std::pair<const void *, size_t>> &ins,
+                const std::vector<std::pair<void *, size_t>> &outs, Work work,
+                const double *hm, const double *hC, ParamLayout layout, int64_t B, int64_t s)
+{
+    HostCtx *c = nullptr;
+    if (int rc = host_ctx(c))
+        return rc;
+    cudaStream_t st = c->st[0];
+    const size_t slots = in_slots + out_slots + 2;
+    unsigned char *pin = nullptr;
+    if (int rc = staging(*c, slots * 8, pin))
+        return rc;
+    unsigned char *dmem = nullptr;
+    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&dmem), slots * 8, st));
+    Scratch guard;  // frees dmem (stream-ordered) on every return path
+    guard.p = reinterpret_cast<double *>(dmem);
+    guard.s = st;
+    size_t off = 0;
+    for (auto &[p, n] : ins) {
+        std::memcpy(pin + off, p, n);
+        off += n;
+    }
+    OSC_CUDA(cudaMemcpyAsync(dmem, pin, in_slots * 8, cudaMemcpyHostToDevice, st));
+    double *d = reinterpret_cast<double *>(dmem);
+    auto *badp = reinterpret_cast<unsigned long long *>(d + in_slots + out_slots);
+    OSC_CUDA(osc::launch_param_check(d + m_off, d + C_off, nparam, badp, st));
+    if (int rc = work(d, st))
+        return rc;
+    OSC_CUDA(cudaMemcpyAsync(pin + in_slots * 8, d + in_slots, (out_slots + 2) * 8,
+                             cudaMemcpyDeviceToHost, st));
+    OSC_CUDA(cudaStreamSynchronize(st));
+    unsigned long long bad[2];
+    std::memcpy(bad, pin + (in_slots + out_slots) * 8, sizeof bad);
+    if (bad[0] != ~0ull || bad[1] != ~0ull)  // the first offender in the caller's layout
+        return host_param_fail(hm, hC, nparam, layout, B, s);
+    off = in_slots * 8;
+    for (auto &[p, n] : outs) {
+        if (p)
+            std::memcpy(p, pin + off, n);
+        off += n;
+    }
+    return OSC_OK;
+}
+
+// Host-pointer form of a batched run.  Small runs are one staged round trip
+// (staged_call).  Large ones are cut into chunks that are pipelined over
+// three streams: chunk c's H2D copy, kernels and D2H copy are ordered on
+// stream c % S, so copies of one chunk overlap the compute of another and
+// consecutive chunks' kernels fill each other's tail waves.  Sampled runs use
+// a single chunk (their [nsamp][...] layout spans the batch).
 int host_run(bool chains, const double *m, const double *C, double *x, double *v, int64_t B,
              int64_t s, double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
              int64_t *first_bad)
@@ -35,7 +154,47 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     const size_t cells = static_cast<size_t>(B * s);
     const size_t bytes = cells * sizeof(double);
     const size_t nsamp = xs ? static_cast<size_t>(1 + nsteps / stride) : 0;
+    const ParamLayout layout = chains ? ParamLayout::Chains : ParamLayout::CellMajor;
 
+    // -- small: one staged round trip --------------------------------------
+    // inputs [m | C | x | v], outputs [x | v | first_bad | worst[2] | xs | vs]
+    const size_t out_slots = 2 * cells + B + 2 + 2 * nsamp * cells;
+    if ((4 * cells + out_slots) * 8 <= kStagedMax) {
+        unsigned long long worst[2] = {~0ull, ~0ull};
+        const size_t sb = nsamp * bytes;
+        auto work = [&](double *d, cudaStream_t st) -> int {
+            double *dm = d, *dC = d + cells, *dx = d + 2 * cells, *dv = d + 3 * cells;
+            double *o = d + 4 * cells;  // the output slots
+            OSC_CUDA(cudaMemcpyAsync(o, dx, 2 * bytes, cudaMemcpyDeviceToDevice, st));
+            double *ox = o, *ov = o + cells;
+            int64_t *fb = reinterpret_cast<int64_t *>(o + 2 * cells);
+            auto *dw = reinterpret_cast<unsigned long long *>(o + 2 * cells + B);
+            double *dxs = xs ? o + 2 * cells + B + 2 : nullptr;
+            double *dvs = xs ? dxs + nsamp * cells : nullptr;
+            int rc = chains ? osc_rk4_chains(dm, dC, ox, ov, B, s, dt, nsteps, stride, dxs, dvs,
+                                             nullptr, fb, 0, OSC_TRUSTED, st)
+                            : osc_rk4_batch2(dm, dC, ox, ov, B, dt, nsteps, stride, dxs, dvs,
+                                             nullptr, fb, OSC_TRUSTED, st);
+            if (rc != OSC_OK)
+                return rc;
+            OSC_CUDA(osc::launch_first_bad(fb, B, dw, st));
+            return OSC_OK;
+        };
+        const int rc = staged_call(
+            4 * cells, out_slots, 0, cells, static_cast<int64_t>(cells),
+            {{m, bytes}, {C, bytes}, {x, bytes}, {v, bytes}},
+            {{x, bytes}, {v, bytes}, {first_bad, B * sizeof(int64_t)}, {worst, sizeof worst},
+             {xs, sb}, {vs, sb}},
+            work, m, C, layout, B, s);
+        if (rc != OSC_OK)
+            return rc;
+        if (worst[0] != ~0ull)
+            return fail(OSC_NONFINITE, "integration diverged at step %lld (system %lld)",
+                        (long long)worst[0], (long long)worst[1]);
+        return OSC_OK;
+    }
+
+    // -- large: chunked multi-stream pipeline ---------------------------------
     // Chunking, so that only the first chunk's H2D and the last one's D2H are
     // exposed: >= 2 MB of state per chunk, at most 8 chunks; 2-DOF chunks
     // keep >= 148*1024 systems so each launch keeps K1's throughput shape.
@@ -50,9 +209,10 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
             nchunk = std::min<int64_t>(n, B);
     }
     const int nstream = static_cast<int>(std::min<int64_t>(nchunk, 3));
-    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
-    for (int i = 0; i < nstream; ++i)
-        OSC_CUDA(cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking));
+    HostCtx *ctx = nullptr;
+    if (int rc = host_ctx(ctx))
+        return rc;
+    cudaStream_t *streams = ctx->st;
     struct Cleanup {
         cudaStream_t *st;
         int n;
@@ -61,11 +221,9 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         {
             for (int i = 0; i < n; ++i)
                 cudaStreamSynchronize(st[i]);  // every stream is done with mem
-            if (mem)
+            if (mem) {
                 cudaFreeAsync(mem, st[0]);
-            for (int i = 0; i < n; ++i) {
-                cudaStreamSynchronize(st[i]);
-                cudaStreamDestroy(st[i]);
+                cudaStreamSynchronize(st[0]);
             }
         }
     } cleanup{streams, nstream};
@@ -89,6 +247,33 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     const auto H2D = cudaMemcpyHostToDevice;
     const auto D2H = cudaMemcpyDeviceToHost;
 
+    // Parameters first: every chunk's m and C go up (in the chunk's device
+    // layout) and are checked in one device pass before any state is copied
+    // or integrated, so an invalid system returns OSC_INVALID with the
+    // caller's buffers untouched (the reference rejects it at construction,
+    // oscillator.py:66-80).  Costs the m/C upload's overlap with compute.
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
+        if (chains) {
+            const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
+            OSC_CUDA(cudaMemcpyAsync(dm + o, m + o, n, H2D, streams[0]));
+            OSC_CUDA(cudaMemcpyAsync(dC + o, C + o, n, H2D, streams[0]));
+        } else {
+            const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
+            for (int r = 0; r < 2; ++r) {
+                OSC_CUDA(cudaMemcpyAsync(dm + o + r * nb, m + r * B + b0, n, H2D, streams[0]));
+                OSC_CUDA(cudaMemcpyAsync(dC + o + r * nb, C + r * B + b0, n, H2D, streams[0]));
+            }
+        }
+    }
+    {
+        int64_t bad[2];
+        if (int rc = scan_params(dm, dC, static_cast<int64_t>(cells), streams[0], bad))
+            return rc;
+        if (bad[0] >= 0 || bad[1] >= 0)  // the first offender in the caller's layout
+            return host_param_fail(m, C, static_cast<int64_t>(cells), layout, B, s);
+    }
+
     for (int64_t c = 0; c < nchunk; ++c) {
         cudaStream_t st = streams[c % nstream];
         const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
@@ -96,12 +281,10 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         if (chains) {
             // [B][s]: a chunk of chains is one contiguous block per array
             const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
-            OSC_CUDA(cudaMemcpyAsync(dm + o, m + o, n, H2D, st));
-            OSC_CUDA(cudaMemcpyAsync(dC + o, C + o, n, H2D, st));
             OSC_CUDA(cudaMemcpyAsync(dx + o, x + o, n, H2D, st));
             OSC_CUDA(cudaMemcpyAsync(dv + o, v + o, n, H2D, st));
             rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps, stride, dxs,
-                                dvs, nullptr, dfb + b0, 0, 0, st);
+                                dvs, nullptr, dfb + b0, 0, OSC_TRUSTED, st);
             if (rc != OSC_OK)
                 return rc;
             OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));
@@ -109,13 +292,13 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         } else {
             // [2][B]: the chunk is packed as its own [2][nb] block on the device
             const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
-            const double *hs[4] = {m, C, x, v};
-            double *ds[4] = {dm, dC, dx, dv};
-            for (int a = 0; a < 4; ++a)
+            const double *hs[2] = {x, v};
+            double *ds[2] = {dx, dv};
+            for (int a = 0; a < 2; ++a)
                 for (int r = 0; r < 2; ++r)
                     OSC_CUDA(cudaMemcpyAsync(ds[a] + o + r * nb, hs[a] + r * B + b0, n, H2D, st));
             rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride, dxs, dvs,
-                                nullptr, dfb + b0, 0, st);
+                                nullptr, dfb + b0, OSC_TRUSTED, st);
             if (rc != OSC_OK)
                 return rc;
             for (int r = 0; r < 2; ++r) {
@@ -150,6 +333,8 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
 
 }  // namespace
 
+extern "C" {
+
 int osc_rk4_batch2_host(const double *m, const double *C, double *x, double *v, int64_t B,
                         double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
                         int64_t *first_bad)
@@ -162,6 +347,47 @@ int osc_rk4_chains_host(const double *m, const double *C, double *x, double *v, 
                         double *vs, int64_t *first_bad)
 {
     return host_run(true, m, C, x, v, B, s, dt, nsteps, stride, xs, vs, first_bad);
+}
+
+int osc_derivative_host(const double *m, const double *C, const double *x, double *dvel,
+                        int64_t B, int64_t s, int cell_major)
+{
+    if (B < 0 || s < 1)
+        return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x || !dvel)
+        return fail(OSC_INVALID, "null buffer");
+    const size_t cells = static_cast<size_t>(B * s), bytes = cells * sizeof(double);
+    auto work = [&](double *d, cudaStream_t st) -> int {
+        OSC_CUDA(osc::launch_derivative(d, d + cells, d + 2 * cells, d + 3 * cells, B, s,
+                                        cell_major != 0, st));
+        return OSC_OK;
+    };
+    return staged_call(3 * cells, cells, 0, cells, static_cast<int64_t>(cells),
+                       {{m, bytes}, {C, bytes}, {x, bytes}}, {{dvel, bytes}}, work, m, C,
+                       cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s);
+}
+
+int osc_energy_host(const double *m, const double *C, const double *x, const double *v,
+                    double *out, int64_t B, int64_t s, int cell_major)
+{
+    if (B < 0 || s < 1)
+        return fail(OSC_INVALID, "need B >= 0 and s >= 1");
+    if (B == 0)
+        return OSC_OK;
+    if (!m || !C || !x || !v || !out)
+        return fail(OSC_INVALID, "null buffer");
+    const size_t cells = static_cast<size_t>(B * s), bytes = cells * sizeof(double);
+    auto work = [&](double *d, cudaStream_t st) -> int {
+        OSC_CUDA(osc::launch_energy(d, d + cells, d + 2 * cells, d + 3 * cells, d + 4 * cells, B,
+                                    s, cell_major != 0, st));
+        return OSC_OK;
+    };
+    return staged_call(4 * cells, static_cast<size_t>(B), 0, cells, static_cast<int64_t>(cells),
+                       {{m, bytes}, {C, bytes}, {x, bytes}, {v, bytes}},
+                       {{out, B * sizeof(double)}}, work, m, C,
+                       cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s);
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 // (include/osc_b200.h is).
 #pragma once
 
+#include <cfloat>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -20,6 +21,10 @@
 namespace osc_capi {
 
 inline thread_local std::string g_last_error;  // one per thread, shared by every capi_*.cu
+// The offending parameter of the calling thread's last error, when it was a
+// parameter-rule violation (osc_last_invalid_parameter); which = -1 otherwise.
+inline thread_local int g_bad_param_which = -1;
+inline thread_local int64_t g_bad_param_index = -1;
 
 inline int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 inline int fail(int code, const char *fmt, ...)
@@ -30,6 +35,8 @@ inline int fail(int code, const char *fmt, ...)
     vsnprintf(buf, sizeof buf, fmt, ap);
     va_end(ap);
     g_last_error = buf;
+    g_bad_param_which = -1;
+    g_bad_param_index = -1;
     return code;
 }
 
@@ -56,6 +63,94 @@ inline int check_run_args(double dt, int64_t nsteps, int64_t stride)
     if (stride < 1)
         return fail(OSC_INVALID, "stride must be >= 1, got %lld", (long long)stride);
     return OSC_OK;
+}
+
+// Flags every integrate entry point accepts.
+constexpr uint32_t kRunFlags = OSC_FMA | OSC_TRUSTED;
+
+// How a flat parameter index maps to (system, cell) for the error message:
+// CellMajor = [s][B] (the batched 2-DOF SoA [2][B]: coordinate i / B of
+// system i % B), Chains = [B][s] (cell i % s of chain i / s).
+enum class ParamLayout { Flat, CellMajor, Chains };
+
+// One device pass of OscillatorSystem's rule (oscillator.py:75-80) over n
+// masses and n spring rates; bad[0] / bad[1] = the smallest offending mass /
+// spring index, -1 if none.  Synchronises `stream`.
+inline int scan_params(const double *m, const double *C, int64_t n, cudaStream_t stream,
+                       int64_t bad[2])
+{
+    bad[0] = bad[1] = -1;
+    if (n <= 0)
+        return OSC_OK;
+    unsigned long long *d = nullptr;
+    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d), 2 * sizeof *d, stream));
+    unsigned long long h[2] = {~0ull, ~0ull};
+    cudaError_t e = osc::launch_param_check(m, C, n, d, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(d, stream);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "param_check_kernel");
+    for (int w = 0; w < 2; ++w)
+        bad[w] = h[w] == ~0ull ? -1 : static_cast<int64_t>(h[w]);
+    return OSC_OK;
+}
+
+// OSC_INVALID naming parameter `which` (0 masses, 1 springs) at flat index
+// gi with value val; recorded for osc_last_invalid_parameter.
+inline int param_fail(int which, int64_t gi, double val, ParamLayout layout, int64_t B,
+                      int64_t s)
+{
+    const char *label = which ? "springs" : "masses";
+    if (layout == ParamLayout::CellMajor)
+        fail(OSC_INVALID, "%s[%lld] = %.17g; must be positive and finite (system %lld)", label,
+             (long long)(gi / B), val, (long long)(gi % B));
+    else if (layout == ParamLayout::Chains)
+        fail(OSC_INVALID, "%s[%lld] = %.17g; must be positive and finite (chain %lld)", label,
+             (long long)(gi % s), val, (long long)(gi / s));
+    else
+        fail(OSC_INVALID, "%s[%lld] = %.17g; must be positive and finite", label,
+             (long long)gi, val);
+    g_bad_param_which = which;
+    g_bad_param_index = gi;
+    return OSC_INVALID;
+}
+
+// Host-side twin for the host-pointer entry points: once the device pass has
+// found an offender, the exact first one in the caller's own layout (masses
+// before springs, lowest index) is located in the caller's host arrays.
+inline int host_param_fail(const double *m, const double *C, int64_t n, ParamLayout layout,
+                           int64_t B = 0, int64_t s = 0)
+{
+    for (int w = 0; w < 2; ++w) {
+        const double *a = w ? C : m;
+        for (int64_t i = 0; i < n; ++i)
+            if (!(a[i] > 0.0 && a[i] <= DBL_MAX))
+                return param_fail(w, i, a[i], layout, B, s);
+    }
+    return fail(OSC_CUDA_ERROR, "parameter check: device and host copies disagree");
+}
+
+// The check every entry point taking device m, C makes before integrating:
+// one coalesced pass, then a synchronisation of `stream` so the call returns
+// OSC_INVALID before enqueuing any work.  Masses are checked before springs,
+// lowest index first -- the reference's order for one system.
+inline int check_params(const double *m, const double *C, int64_t n, cudaStream_t stream,
+                        ParamLayout layout = ParamLayout::Flat, int64_t B = 0, int64_t s = 0)
+{
+    int64_t bad[2];
+    if (int rc = scan_params(m, C, n, stream, bad))
+        return rc;
+    const int which = bad[0] >= 0 ? 0 : (bad[1] >= 0 ? 1 : -1);
+    if (which < 0)
+        return OSC_OK;
+    double val = 0.0;
+    OSC_CUDA(cudaMemcpyAsync(&val, (which ? C : m) + bad[which], sizeof val,
+                             cudaMemcpyDeviceToHost, stream));
+    OSC_CUDA(cudaStreamSynchronize(stream));
+    return param_fail(which, bad[which], val, layout, B, s);
 }
 
 inline osc::StepConsts consts(double dt)

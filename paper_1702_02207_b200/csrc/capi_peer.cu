@@ -197,7 +197,7 @@ int osc_rk4_chain_sharded(int ngpu, const int *devs, const double *m, const doub
                           double *v, int64_t s, double dt, int64_t nsteps, int64_t halo_steps,
                           int64_t *first_bad, uint32_t flags)
 {
-    if (flags & ~uint32_t(OSC_FMA))
+    if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, 1))
         return rc;
@@ -254,6 +254,22 @@ int osc_rk4_chain_sharded(int ngpu, const int *devs, const double *m, const doub
         OSC_CUDA(cudaMemcpyAsync(r.v2, v + r.blo, r.n * D, cudaMemcpyHostToDevice, r.st));
         OSC_CUDA(cudaEventRecord(r.ev[1], r.st));  // "period -1" done: the uploads
     }
+    // the parameter rule (oscillator.py:66-80), one device pass per shard;
+    // the exact first offender is then located in the caller's arrays
+    if (!(flags & OSC_TRUSTED)) {
+        bool any = false;
+        for (auto &r : set.sh) {
+            OSC_CUDA(cudaSetDevice(r.dev));
+            int64_t bad[2];
+            if (int rc = scan_params(r.m, r.C, r.n, r.st, bad))
+                return rc;
+            any = any || bad[0] >= 0 || bad[1] >= 0;
+        }
+        if (any)
+            return host_param_fail(m, C, s, ParamLayout::Flat);
+    }
+    flags |= OSC_TRUSTED;  // per-period launches below skip the check
+
     // neighbours on other devices store into each other's memory over NVLink
     for (int i = 0; i + 1 < ngpu; ++i) {
         const int a = set.sh[i].dev, b = set.sh[i + 1].dev;

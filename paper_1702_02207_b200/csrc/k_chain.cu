@@ -560,11 +560,17 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
 cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream)
 {
     // Tiled runs of the default shape go through the persistent prefetching
-    // kernel when the bulk copies are 16-byte aligned (even offsets).
+    // kernel when the bulk copies are 16-byte aligned: even cell offsets AND
+    // 16-byte aligned base pointers (a caller may pass any 8-byte aligned
+    // view, e.g. a tensor with an odd storage offset); otherwise the plain
+    // tiled kernel, same bytes.
     const int64_t TILE = int64_t(threads) * K;
     const bool tiled = g.H > 0 || g.tiles > 1;
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     const bool aligned = (g.n % 2 == 0) && (g.own_lo % 2 == 0) && (g.own_hi % 2 == 0) &&
-                         (g.W % 2 == 0) && (g.H % 2 == 0) && g.n >= TILE;
+                         (g.W % 2 == 0) && (g.H % 2 == 0) && g.n >= TILE && a16(g.m) &&
+                         a16(g.C) && a16(g.xin) && a16(g.vin) && a16(g.xout) && a16(g.vout) &&
+                         (!g.xs || (a16(g.xs) && a16(g.vs)));
     static const bool disable = std::getenv("OSC_NO_PERSIST") != nullptr;
     if (tiled && aligned && !disable) {
         if (K == 8 && threads == 128)

@@ -6,6 +6,7 @@
 #include "osc_kernels.h"
 
 #include <algorithm>
+#include <cfloat>
 
 namespace osc {
 namespace {
@@ -295,6 +296,39 @@ __global__ void first_bad_index_kernel(const int64_t *__restrict__ fb, int64_t B
 }
 
 }  // namespace
+
+// OscillatorSystem's parameter rule (oscillator.py:75-80) over n masses and
+// n spring rates: out[0] / out[1] = the smallest index of a mass / spring
+// rate that is not positive and finite (NaN, +-Inf, <= 0, -0.0), ~0 if none.
+// One coalesced pass; atomics only on offenders.
+__global__ void param_check_kernel(const double *__restrict__ m, const double *__restrict__ C,
+                                   int64_t n, unsigned long long *out)
+{
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double a = m[i], b = C[i];
+        if (!(a > 0.0 && a <= DBL_MAX))
+            atomicMin(&out[0], static_cast<unsigned long long>(i));
+        if (!(b > 0.0 && b <= DBL_MAX))
+            atomicMin(&out[1], static_cast<unsigned long long>(i));
+    }
+}
+
+cudaError_t launch_param_check(const double *m, const double *C, int64_t n,
+                               unsigned long long *out, cudaStream_t stream)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 8, (n + 255) / 256)));
+    cudaError_t e = cudaMemsetAsync(out, 0xff, 2 * sizeof(unsigned long long), stream);
+    if (e != cudaSuccess)
+        return e;
+    if (n > 0)
+        param_check_kernel<<<grid, 256, 0, stream>>>(m, C, n, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *out,
                              cudaStream_t stream)

@@ -68,6 +68,11 @@ cudaError_t launch_energy(const double *m, const double *C, const double *x, con
 cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *out,
                              cudaStream_t stream);
 
+// Parameter rule of OscillatorSystem (oscillator.py:75-80): out[0] / out[1]
+// = smallest index of an invalid mass / spring rate (~0 when none).
+cudaError_t launch_param_check(const double *m, const double *C, int64_t n,
+                               unsigned long long *out, cudaStream_t stream);
+
 cudaError_t launch_div2_classify(const double *b, int64_t n, uint8_t *pass, cudaStream_t stream);
 
 cudaError_t launch_check_division(int64_t n, uint64_t seed, int mode,

@@ -9,6 +9,32 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
+# The unmodified reference package: the install under baseline/_ref
+# (scripts/install_reference.sh; travels to the GPU box) or, in the build
+# container only, the read-only source tree.
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+REF_SOURCE = "/root/reference/pkg/src"
+
+
+def reference_path():
+    """Directory to put on sys.path to import ``oscbench``, or None."""
+    for cand in (REF_INSTALL, REF_SOURCE):
+        if os.path.isfile(os.path.join(cand, "oscbench", "__init__.py")):
+            return cand
+    return None
+
+
+def import_reference():
+    """Import the reference package ``oscbench`` (or None when absent)."""
+    path = reference_path()
+    if path is None:
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import oscbench
+
+    return oscbench
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libosc_b200.so")

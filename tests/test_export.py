@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import paper_1702_02207_b200 as osc
+from conftest import import_reference
 from paper_1702_02207_b200 import export
 
 
@@ -24,11 +25,9 @@ def test_csv_matches_reference_exporter(golden, tmp_path, name):
     traj = _traj(golden, name)
     ours = tmp_path / "ours.csv"
     export.export_trajectory(traj, str(ours))
-    ref_src = "/root/reference/pkg/src"
-    if not os.path.isdir(ref_src):  # pragma: no cover - GPU box
+    oscbench = import_reference()
+    if oscbench is None:  # pragma: no cover - run scripts/install_reference.sh
         pytest.skip("reference package not present")
-    sys.path.insert(0, ref_src)
-    import oscbench
     from oscbench.harness import export_trajectory as ref_export
 
     theirs = tmp_path / "theirs.csv"

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import bits
+from conftest import bits, import_reference, reference_path
 from paper_1702_02207_b200 import workloads
 from paper_1702_02207_b200.oscillator import accumulated_times
 
@@ -157,21 +157,18 @@ def test_dense_restatement_tracks_analytic():
 # the reference package is not on the GPU box)
 # --------------------------------------------------------------------------
 
-import os  # noqa: E402
-import sys  # noqa: E402
 
 from hypothesis import given, settings, strategies as st  # noqa: E402
 
-_REF = "/root/reference/pkg/src"
+_REF = reference_path()
 
 
-@pytest.mark.skipif(not os.path.isdir(_REF), reason="reference package not present")
+@pytest.mark.skipif(_REF is None, reason="reference package not present")
 @settings(max_examples=40, deadline=None, derandomize=True)
 @given(s=st.integers(1, 9), nsteps=st.integers(1, 60), stride=st.integers(1, 7),
        seed=st.integers(0, 2**32 - 1), dt=st.sampled_from([1e-4, 1e-3, 5e-3, 2e-2]))
 def test_c_oracle_equals_reference_on_random_chains(s, nsteps, stride, seed, dt):
-    sys.path.insert(0, _REF)
-    import oscbench
+    oscbench = import_reference()
 
     rng = np.random.default_rng(seed)
     m = rng.uniform(0.3, 3.0, s)

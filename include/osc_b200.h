@@ -50,7 +50,7 @@ extern "C" {
 #define OSC_INVALID 2
 #define OSC_CUDA_ERROR 3
 
-#define OSC_ABI_VERSION 10
+#define OSC_ABI_VERSION 11
 
 /* flags: OSC_FMA selects the opt-in FMA mode -- a*b+c contracted and x/m
  * computed as x*(1/m).  Roughly half the FP64 instructions, NOT bit-identical
@@ -153,6 +153,39 @@ typedef struct {
     int64_t count;
 } osc_peer_t;
 
+/* In-kernel ordering of a shard's launches with its neighbours (the fused
+ * exchange between processes, one per GPU).  Only the tiles next to a ghost
+ * zone depend on a neighbour; with a sync descriptor they run after the
+ * interior tiles, and before one touches its inputs its CTA waits ON THE
+ * DEVICE until the neighbour's edge counter facing us has reached `period`
+ * (the neighbour's previous period stored our ghosts and finished reading the
+ * buffer we are about to store into); the last edge tile of a side then
+ * posts period + 1 into our counter for that side.  No host involvement and
+ * no stream-level wait per period.
+ *   ready[0] / ready[1]: the left / right neighbour's counter facing us (its
+ *     counters[1] / counters[0]), mapped peer memory; NULL = no neighbour.
+ *   counters: ours, 8 x uint64 device memory zeroed before the first launch:
+ *     [0] / [1] our left / right edge done through period q (= q + 1),
+ *     [2] / [3] internal tallies, [4..7] the timeout record
+ *     {flag, period, side (0 left, 1 right), counter value seen}.
+ *   period: q, counted over all launches since the counters were zeroed.
+ *   timeout_ns: bound of every wait.  On expiry the record is written, no
+ *     later wait (this launch or any other on these counters) blocks, the
+ *     launch completes -- its results are garbage -- and the caller reads
+ *     the record (osc_edge_sync_status) and fails instead of hanging. */
+typedef struct {
+    const uint64_t *ready[2];
+    uint64_t *counters;
+    uint64_t period;
+    int64_t timeout_ns;
+} osc_edge_sync_t;
+
+/* Copy the timeout record of `counters` to record[4] (host) after the
+ * stream's work is done: returns OSC_OK if no wait timed out, else
+ * OSC_CUDA_ERROR with osc_last_error() naming the period, the side and the
+ * counter value seen. */
+int osc_edge_sync_status(const uint64_t *counters, uint64_t *record, void *stream);
+
 /* One temporally blocked launch over a chain shard buffer of n cells, used by
  * the multi-GPU driver: cells [own_lo, own_hi) are advanced nsteps steps from
  * (xin, vin) into (xout, vout); the cells outside are ghosts of the
@@ -161,12 +194,15 @@ typedef struct {
  * harmless as long as each ghost zone is at least 2*nsteps cells wide.
  * left/right (may be NULL): write our boundary cells straight into the
  * neighbours' next-input ghost zones (no separate exchange).
+ * sync (may be NULL): order the edge tiles with the neighbours on the device
+ * (osc_edge_sync_t); NULL = the caller orders launches (streams / events).
  * first_bad: [1], updated to the minimum bad step (global step0 + j). */
 int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           const double *vin, double *xout, double *vout, int64_t n,
                           int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
                           int64_t step0, int64_t *first_bad, const osc_peer_t *left,
-                          const osc_peer_t *right, uint32_t flags, void *stream);
+                          const osc_peer_t *right, const osc_edge_sync_t *sync, uint32_t flags,
+                          void *stream);
 
 /* Stream-ordered 64-bit counters, for ordering work across processes
  * without host synchronisation: osc_stream_write_u64 stores value at addr

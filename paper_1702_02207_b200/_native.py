@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 
 OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
-ABI_VERSION = 10
+ABI_VERSION = 11
 OSC_FMA = 1
 OSC_TRUSTED = 2
 
@@ -41,8 +41,9 @@ SIGNATURES = {
     "osc_rk4_chains": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _i64, _i64, _vp,
                                       _vp, _vp, _vp, _i64, ctypes.c_uint32, _vp]),
     "osc_rk4_chain_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
-                                             _dbl, _i64, _i64, _vp, _vp, _vp, ctypes.c_uint32,
-                                             _vp]),
+                                             _dbl, _i64, _i64, _vp, _vp, _vp, _vp,
+                                             ctypes.c_uint32, _vp]),
+    "osc_edge_sync_status": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_uint64), _vp]),
     "osc_stream_write_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_stream_wait_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_chain_plan": (ctypes.c_int, [_i64, _i64, _i64, _i64, _vp]),
@@ -84,6 +85,14 @@ class Peer(ctypes.Structure):
 
     _fields_ = [("x", ctypes.c_void_p), ("v", ctypes.c_void_p), ("offset", ctypes.c_int64),
                 ("count", ctypes.c_int64)]
+
+
+class EdgeSync(ctypes.Structure):
+    """osc_edge_sync_t: device-side ordering of a shard's edge tiles with its
+    neighbours (ready: the neighbours' counters facing us; counters: ours)."""
+
+    _fields_ = [("ready", ctypes.c_void_p * 2), ("counters", ctypes.c_void_p),
+                ("period", ctypes.c_uint64), ("timeout_ns", ctypes.c_int64)]
 
 
 class NativeUnavailableError(RuntimeError):

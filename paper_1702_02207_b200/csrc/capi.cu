@@ -249,8 +249,8 @@ int osc_chain_plan(int64_t B, int64_t s, int64_t nsteps, int64_t halo_steps, int
 int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, const double *vin,
                           double *xout, double *vout, int64_t n, int64_t own_lo, int64_t own_hi,
                           double dt, int64_t nsteps, int64_t step0, int64_t *first_bad,
-                          const osc_peer_t *left, const osc_peer_t *right, uint32_t flags,
-                          void *stream)
+                          const osc_peer_t *left, const osc_peer_t *right,
+                          const osc_edge_sync_t *sync, uint32_t flags, void *stream)
 {
     if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
@@ -297,8 +297,35 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
         const int64_t lo = side == 0 ? own_lo : own_hi - p->count;
         g.peer[side] = osc::PeerGhost{p->x, p->v, p->offset, lo, lo + p->count};
     }
+    if (sync) {
+        if (!sync->counters || sync->timeout_ns < 0)
+            return fail(OSC_INVALID, "bad edge sync descriptor");
+        g.sync.ready[0] = sync->ready[0];
+        g.sync.ready[1] = sync->ready[1];
+        g.sync.ctr = sync->counters;
+        g.sync.period = sync->period;
+        g.sync.timeout_ns = sync->timeout_ns;
+        edge_sets(g, kTileK * kTileThreads, g.sync.nedge);
+    }
     cudaError_t e = osc::launch_chain(g, kTileK, kTileThreads, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "chain_rk4_kernel");
+}
+
+int osc_edge_sync_status(const uint64_t *counters, uint64_t *record, void *stream)
+{
+    if (!counters || !record)
+        return fail(OSC_INVALID, "null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    OSC_CUDA(cudaMemcpyAsync(record, counters + 4, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                             st));
+    OSC_CUDA(cudaStreamSynchronize(st));
+    if (record[0] == 0)
+        return OSC_OK;
+    return fail(OSC_CUDA_ERROR,
+                "edge sync timed out: period %llu waited for the %s neighbour's counter to reach "
+                "%llu, saw %llu",
+                (unsigned long long)record[1], record[2] ? "right" : "left",
+                (unsigned long long)record[1], (unsigned long long)record[3]);
 }
 
 int osc_rowscale(const double *K, const double *m, double *A, int64_t s, void *stream)

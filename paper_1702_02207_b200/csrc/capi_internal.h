@@ -271,6 +271,50 @@ inline int plan_chain(int64_t s, int64_t B, int64_t nsteps, int64_t halo_steps, 
     return OSC_OK;
 }
 
+// The edge-tile sets of a sharded launch (osc::EdgeSync::nedge): how many
+// leading tiles read the left ghost zone or store into the left neighbour,
+// and how many trailing tiles do so on the right.  Tile geometry as the
+// kernels compute it (k_chain.cu tile_geom / chain_rk4_kernel): owned
+// [own_lo + t*W, +W), input from own_start - H (clamped at 0; slid left to
+// end at the buffer end when the tile fits the buffer).  Both sets are
+// contiguous because own_start grows with t.
+inline void edge_sets(const osc::SegArgs &g, int64_t TILE, int64_t nedge[2])
+{
+    auto input = [&](int64_t t, int64_t &L, int64_t &end, int64_t &os, int64_t &oe) {
+        os = g.own_lo + t * g.W;
+        oe = std::min(os + g.W, g.own_hi);
+        L = std::max<int64_t>(0, os - g.H);
+        if (TILE <= g.n && L + TILE > g.n)
+            L = g.n - TILE;
+        end = std::min(L + TILE, g.n);
+    };
+    auto involved = [&](int64_t t, int side) {
+        int64_t L, end, os, oe;
+        input(t, L, end, os, oe);
+        const osc::PeerGhost &p = g.peer[side];
+        const bool writes = p.x && os < p.hi && oe > p.lo;
+        const bool reads = side == 0 ? L < g.own_lo : end > g.own_hi;
+        return writes || reads;
+    };
+    nedge[0] = nedge[1] = 0;
+    for (int side = 0; side < 2; ++side) {
+        if (!g.sync.ready[side] && !g.peer[side].x)
+            continue;  // no neighbour on this side
+        auto tile_at = [&](int64_t i) { return side == 0 ? i : g.tiles - 1 - i; };
+        // the run of involved tiles from this side's end (own_start grows with
+        // the tile, so the involvement of ordinary tiles ends with the run) ...
+        int64_t k = 0;
+        while (k < g.tiles && involved(tile_at(k), side))
+            ++k;
+        // ... except on tiny shards, where the slid last tile or a padded
+        // first tile can reach the far ghost zone: then every tile counts
+        for (int64_t i = std::max(k, g.tiles - 2); i < g.tiles; ++i)
+            if (involved(tile_at(i), side))
+                k = g.tiles;
+        nedge[side] = k;
+    }
+}
+
 // Keep freed stream-ordered allocations in the device's default pool instead
 // of returning them to the driver at every synchronisation (the default
 // release threshold is 0), so repeated host-API calls do not re-map memory.

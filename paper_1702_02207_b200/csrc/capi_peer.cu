@@ -311,7 +311,8 @@ int osc_rk4_chain_sharded(int ngpu, const int *devs, const double *m, const doub
             if (int rc = osc_rk4_chain_advance(r.m, r.C, r.x, r.v, r.x2, r.v2, r.n, r.own_lo,
                                                r.own_hi, dt, n, k, r.fb,
                                                i > 0 ? &left : nullptr,
-                                               i + 1 < ngpu ? &right : nullptr, flags, r.st))
+                                               i + 1 < ngpu ? &right : nullptr, nullptr, flags,
+                                               r.st))
                 return rc;
             OSC_CUDA(cudaEventRecord(r.ev[p % 2], r.st));
         }

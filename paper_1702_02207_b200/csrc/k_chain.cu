@@ -112,6 +112,116 @@ __device__ __forceinline__ bool diverged_before(const SegArgs &g, int64_t buf)
     return fb != 0 && fb <= g.step0;
 }
 
+// ---------------------------------------------------------------------------
+// Edge-tile ordering with the neighbouring shards (EdgeSync, the fused
+// exchange of the multi-process peer transport).  Only the tiles next to a
+// ghost zone depend on a neighbour: they read ghosts the neighbour's previous
+// period stored into our buffer and store our boundary cells into the buffer
+// the neighbour reads next.  So the interior tiles run first without any
+// ordering, and each edge tile's thread 0 waits -- bounded, on the device --
+// until the neighbour's edge counter shows its previous period's edge done;
+// the last edge tile of a side then posts ours.  In steady state the wait is
+// already satisfied when an edge tile comes up; a neighbour that stops
+// making progress turns into a timeout record instead of a hang.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
+{
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Position `it` of a buffer's tile walk -> tile index: with edge sync the
+// interior tiles first, then the left-edge set, then the right-edge set.
+__device__ __forceinline__ int64_t tile_order(const SegArgs &g, int64_t it)
+{
+    if (!g.sync.ctr)
+        return it;
+    const int64_t a = g.sync.nedge[0], b = g.sync.nedge[1];
+    const int64_t rs = max(a, g.tiles - b);  // first tile of the right set
+    const int64_t nint = rs - a;              // interior tiles (>= 0)
+    if (it < nint)
+        return a + it;
+    const int64_t j = it - nint;
+    return j < a ? j : rs + (j - a);
+}
+
+// Bit 0: the tile involves the left neighbour, bit 1: the right one.
+__device__ __forceinline__ int edge_sides(const SegArgs &g, int64_t tile)
+{
+    if (!g.sync.ctr)
+        return 0;
+    return (tile < g.sync.nedge[0] ? 1 : 0) | (tile >= g.tiles - g.sync.nedge[1] ? 2 : 0);
+}
+
+// Thread 0, before an edge tile touches its inputs: wait until each involved
+// neighbour's counter reaches `period`.  After timeout_ns the first waiter
+// records {1, period, side, value seen} in ctr[4..7]; from then on nobody
+// waits (the launch drains, its results are garbage, the host raises).
+__device__ void edge_wait(const EdgeSync &s, int sides)
+{
+    for (int side = 0; side < 2; ++side) {
+        const uint64_t *r = s.ready[side];
+        if (!((sides >> side) & 1) || !r)
+            continue;
+        uint64_t t0 = 0;
+        for (uint32_t spin = 0;; ++spin) {
+            const uint64_t c = ld_acquire_sys(r);
+            if (static_cast<int64_t>(c - s.period) >= 0)
+                break;
+            if (*reinterpret_cast<volatile uint64_t *>(&s.ctr[4]) != 0)
+                break;  // a wait has already timed out: drain
+            const uint64_t now = globaltimer_ns();
+            if (spin == 0) {
+                t0 = now;
+            } else if (static_cast<int64_t>(now - t0) > s.timeout_ns) {
+                auto *flag = reinterpret_cast<unsigned long long *>(&s.ctr[4]);
+                if (atomicCAS(flag, 0ull, 1ull) == 0ull) {
+                    s.ctr[5] = s.period;
+                    s.ctr[6] = static_cast<uint64_t>(side);
+                    s.ctr[7] = c;
+                    __threadfence_system();
+                }
+                break;
+            }
+            __nanosleep(128);
+        }
+    }
+    // the bulk (async-proxy) reads that follow must see the peers' stores
+    asm volatile("fence.proxy.async;" ::: "memory");
+}
+
+// Thread 0, after every thread of an edge tile has stored (and fenced) its
+// cells: count the tile; the last edge tile of a side resets the tally for
+// the next launch and posts period + 1.
+__device__ void edge_done(const EdgeSync &s, int sides)
+{
+    for (int side = 0; side < 2; ++side) {
+        if (!((sides >> side) & 1) || s.nedge[side] == 0)
+            continue;
+        unsigned long long old;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                     : "=l"(old)
+                     : "l"(&s.ctr[2 + side])
+                     : "memory");
+        if (static_cast<int64_t>(old) + 1 == s.nedge[side]) {
+            s.ctr[2 + side] = 0;  // the next launch is stream-ordered after this one
+            __threadfence_system();
+            st_release_sys(&s.ctr[side], s.period + 1);
+        }
+    }
+}
+
 // Zero every slot (sentinels included); callers then __syncthreads().
 __device__ __forceinline__ void edges_init(Edges &e)
 {
@@ -224,15 +334,22 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     __shared__ Edges edges;
     __shared__ int s_skip;
     const int64_t buf_id = blockIdx.x / g.tiles;
-    const int64_t tile = blockIdx.x % g.tiles;
+    const int64_t tile = tile_order(g, blockIdx.x % g.tiles);
+    const int sides = edge_sides(g, tile);
     // One read, broadcast: another CTA may record a divergence at any time,
     // and the exit must be uniform across this CTA's barriers.
     edges_init(edges);
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
         s_skip = diverged_before(g, buf_id);
+        if (sides && !s_skip)
+            edge_wait(g.sync, sides);
+    }
     __syncthreads();
-    if (s_skip)
+    if (s_skip) {
+        if (threadIdx.x == 0 && sides)
+            edge_done(g.sync, sides);  // nothing stored, but the neighbours must not stall
         return;  // already diverged: state is unspecified, as integrate raised
+    }
 
     const int64_t TILE = static_cast<int64_t>(blockDim.x) * K;
     const int64_t own_start = g.own_lo + tile * g.W;
@@ -291,6 +408,12 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
         const int64_t c = c0 + j;
         if (c >= own_start && c < own_end)
             store_owned(g, base, c, x[j], v[j]);
+    }
+    if (sides) {
+        __threadfence_system();  // our peer stores, before the post
+        __syncthreads();
+        if (threadIdx.x == 0)
+            edge_done(g.sync, sides);
     }
 }
 
@@ -359,13 +482,15 @@ __device__ __forceinline__ void store_peers(const SegArgs &g, int64_t c, double 
 
 struct TileGeom {
     int64_t buf_id, base, L, own_start, own_end;
+    int sides;  // edge-sync sides of the tile (edge_sides)
 };
 
 __device__ __forceinline__ TileGeom tile_geom(const SegArgs &g, int64_t it, int64_t TILE)
 {
     TileGeom tg;
     tg.buf_id = it / g.tiles;
-    const int64_t tile = it % g.tiles;
+    const int64_t tile = tile_order(g, it % g.tiles);
+    tg.sides = edge_sides(g, tile);
     tg.own_start = g.own_lo + tile * g.W;
     tg.own_end = min(tg.own_start + g.W, g.own_hi);
     tg.L = max(static_cast<int64_t>(0), tg.own_start - g.H);
@@ -382,6 +507,8 @@ __device__ __forceinline__ void issue_tile(const SegArgs &g, int64_t it, double 
     constexpr int64_t TILE = int64_t(NT) * K;
     constexpr unsigned bytes = TILE * sizeof(double);
     const TileGeom tg = tile_geom(g, it, TILE);
+    if (tg.sides)  // an edge tile reads ghosts the neighbour stores: wait for them
+        edge_wait(g.sync, tg.sides);
     const int64_t o = tg.base + tg.L;
     mbar_expect_tx(bar, 4 * bytes);
     bulk_g2s(dst, g.m + o, bytes, bar);
@@ -479,10 +606,14 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 if (c >= tg.own_start && c < tg.own_end)
                     store_peers(g, c, x[j], v[j]);
             }
+            if (tg.sides)
+                __threadfence_system();  // our peer stores, before the post
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();  // every thread is done with buffer b; the results are in it
         if (threadIdx.x == 0) {
+            if (tg.sides)  // post before waiting for the next tile (no wait cycle)
+                edge_done(g.sync, tg.sides);
             if (!s_skip) {
                 const int64_t o = tg.own_start - tg.L;
                 const unsigned bytes = static_cast<unsigned>(tg.own_end - tg.own_start) * 8u;

@@ -16,6 +16,21 @@ struct PeerGhost {
     int64_t offset, lo, hi;
 };
 
+// In-kernel ordering of a shard's edge tiles with its neighbouring shards
+// (the multi-process fused exchange; include/osc_b200.h osc_edge_sync_t).
+// Tiles [0, nedge[0]) read the left ghost zone or store into the left
+// neighbour, tiles [tiles - nedge[1], tiles) likewise on the right; they run
+// LAST (interior tiles first), wait (bounded) until the neighbour's edge
+// counter reaches `period` before touching anything, and the last of them on
+// a side posts period + 1 into our counter for that side.
+struct EdgeSync {
+    const uint64_t *ready[2];  // neighbours' edge counters facing us (peer memory)
+    uint64_t *ctr;             // ours: [0],[1] edge done; [2],[3] tallies; [4..7] timeout record
+    uint64_t period;
+    int64_t timeout_ns;
+    int64_t nedge[2];
+};
+
 // One launch of the chain kernel over nbuf buffers of n cells each.
 struct SegArgs {
     const double *m, *C;     // [nbuf][n]
@@ -31,6 +46,7 @@ struct SegArgs {
     int64_t nsteps, step0;
     bool fma;                // OSC_FMA mode (not bit-identical)
     PeerGhost peer[2];       // left / right neighbour ghost targets (x == nullptr: none)
+    EdgeSync sync;           // sync.ctr == nullptr: no in-kernel ordering (stream/event order)
 };
 
 // Fused compare (modal.py:141-162) at every retained sample of K1: ts are

@@ -95,6 +95,20 @@ class IpcEvent:
             self.ev = 0
 
 
+def edge_sync_status(counters_ptr: int, stream: torch.cuda.Stream):
+    """The timeout record of an edge-sync counter block after ``stream``'s
+    work is done: None, or (period, side, value seen) of the wait that
+    expired (osc_edge_sync_status)."""
+    rec = (ctypes.c_uint64 * 4)()
+    rc = _native.lib().osc_edge_sync_status(ctypes.c_void_p(counters_ptr), rec,
+                                            ctypes.c_void_p(stream.cuda_stream))
+    if rc == _native.OSC_OK:
+        return None
+    if rec[0] == 0:
+        _check(rc, "osc_edge_sync_status")
+    return int(rec[1]), int(rec[2]), int(rec[3])
+
+
 def stream_write_u64(stream: torch.cuda.Stream, ptr: int, value: int):
     """Store value at ptr once all prior work of stream is done (fenced)."""
     _check(_native.lib().osc_stream_write_u64(ctypes.c_void_p(stream.cuda_stream),

@@ -20,24 +20,45 @@ Two transports:
 * ``"peer"``: the fused compute + exchange.  Each rank maps its neighbours'
   state buffers (CUDA IPC; NVLink peer memory between GPUs) and the tile
   kernel itself stores its boundary cells into the neighbours' next-input
-  ghost zones (``osc_peer_t``), so there is no exchange step at all.  Order is
-  kept on the device only: after its period-p launch a rank's stream stores
-  p + 1 into its period counter (``osc_stream_write_u64``, fenced after the
-  kernel's peer stores), and before period p its stream waits until each
-  neighbour's counter reaches p (``osc_stream_wait_u64``) -- the neighbour's
-  period p-1 both produced our ghosts and finished reading the buffer we are
-  about to write into (ping-pong buffers, parity from the global period
-  count).  The waits happen in the GPU front-end: no host barrier per period,
-  and no kernel ever waits on another GPU.
+  ghost zones (``osc_peer_t``), so there is no exchange step at all.  Order
+  is kept on the device, per edge tile (``osc_edge_sync_t``): only the tiles
+  next to a ghost zone depend on a neighbour, so each period's launch runs
+  its interior tiles first, and an edge tile's CTA waits -- bounded, in the
+  kernel -- until the neighbour's edge counter shows that the neighbour's
+  previous period stored our ghosts and finished reading the buffer we store
+  into (ping-pong buffers, parity from the global period count); the last
+  edge tile of a side then posts our counter.  One launch per period, no
+  stream-level wait, no host barrier.  A neighbour that stops making
+  progress turns into a timeout record (``OSC_PEER_TIMEOUT_MS``, default
+  30 s): the launch drains and ``run`` raises :class:`PeerTimeoutError`
+  naming the rank, the period, the side and the counter value seen --
+  instead of hanging (the reference guards its barrier the same way,
+  parallel.py:205-255).
 """
 
 from __future__ import annotations
 
+import json
 import os
+import time
 from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
+
+
+class PeerTimeoutError(RuntimeError):
+    """A neighbour's edge counter did not reach the awaited period in time
+    (the fused exchange's bounded wait, osc_edge_sync_t)."""
+
+    def __init__(self, rank, period, side, seen, trace):
+        self.rank, self.period, self.side, self.seen = rank, period, side, seen
+        self.trace = trace
+        nb = rank - 1 if side == 0 else rank + 1
+        super().__init__(
+            f"rank {rank}: period {period} waited for rank {nb}'s "
+            f"{'right' if side == 0 else 'left'} edge counter to reach {period}, saw {seen} "
+            f"(last phases: {trace[-6:]})")
 
 
 def partition(s: int, rank: int, world: int) -> tuple[int, int]:
@@ -80,11 +101,13 @@ def layout(s: int, rank: int, world: int, halo_steps: int) -> ShardLayout:
 
 
 def _cuda_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None, left=None, right=None):
+                  stream=None, left=None, right=None, sync=None):
     from . import batched
 
+    # the shard's parameters were validated once at construction
     batched.chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
-                          first_bad, stream=stream, left=left, right=right)
+                          first_bad, stream=stream, left=left, right=right, trusted=True,
+                          sync=sync)
 
 
 class ShardedChain:
@@ -99,7 +122,7 @@ class ShardedChain:
     EDGE_CELLS = 4096  # >= any tile (K x threads) so interior tiles never slide into ghosts
 
     def __init__(self, m, C, x0, v0, dt, *, halo_steps=32, group=None, device=None,
-                 advance=None, rank=None, world=None, transport="nccl"):
+                 advance=None, rank=None, world=None, transport="nccl", timeout_ms=None):
         if transport not in ("nccl", "peer"):
             raise ValueError(f"transport must be 'nccl' or 'peer', got {transport!r}")
         self.transport = transport
@@ -135,8 +158,44 @@ class ShardedChain:
         self.cuda = self.device.type == "cuda"
         self.comm_stream = torch.cuda.Stream(self.device) if self.cuda else None
         self.peer_bufs = {}  # neighbour rank -> ((x, v) of its buffer 0, (x, v) of buffer 1, blo)
+        self._t0 = time.monotonic()
+        self.trace = []
+        if timeout_ms is None:
+            timeout_ms = float(os.environ.get("OSC_PEER_TIMEOUT_MS", "30000"))
+        self.timeout_ns = int(timeout_ms * 1e6)
+        if self.cuda and self.advance is _cuda_advance:
+            self._validate(distributed)
         if transport == "peer" and self.world > 1 and dist.is_initialized() and distributed:
             self._setup_peer()
+
+    def _validate(self, distributed):
+        """The parameter rule (oscillator.py:66-80) once, over the whole chain:
+        each rank checks its buffer on the device (osc_validate_parameters),
+        the ranks agree on the first offender (min over ranks of the global
+        index; masses before springs), and every rank raises the same
+        NonPositiveParameterError -- no rank is left waiting in a collective.
+        Per-period launches then skip the check (OSC_TRUSTED)."""
+        from . import _native, batched
+        from .oscillator import NonPositiveParameterError
+
+        big = 1 << 62
+        found = [big, big]  # masses, springs (global cell index)
+        try:
+            batched.validate_parameters(self.m, self.C)
+        except NonPositiveParameterError:
+            which, idx = _native.last_invalid_parameter()
+            found[which] = self.L.blo + idx
+        if distributed and self.world > 1:
+            t = torch.tensor(found, dtype=torch.int64)
+            group = getattr(self, "host_group", None) or self.group
+            if dist.get_backend(group) == "nccl":
+                t = t.to(self.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            found = [int(u) for u in t.cpu()]
+        for which, label in ((0, "masses"), (1, "springs")):
+            if found[which] < big:
+                raise NonPositiveParameterError(
+                    f"{label}[{found[which]}]: must be positive and finite")
 
     # -- fused exchange over peer memory --------------------------------------
     def peer_descriptors(self, p):
@@ -157,52 +216,44 @@ class ShardedChain:
         return tuple(out)
 
     def _setup_peer(self):
-        """Own state and period counter in exportable allocations; map the
+        """Own state and edge counters in exportable allocations; map the
         neighbours' (CUDA IPC: NVLink peer memory between GPUs)."""
         from . import peer
 
+        self._phase("peer-setup")
         self.host_group = dist.new_group(backend="gloo")
-        self.peer_counters = {}
         n = self.L.n
         self._own = [peer.DeviceVector(n, self.device) for _ in range(4)]
         for dst, src in zip(self._own, (self.x, self.v, self.x2, self.v2)):
             dst.tensor.copy_(src)
         self.x, self.v, self.x2, self.v2 = (b.tensor for b in self._own)
-        # period counter: our stream stores p + 1 after our period p; the
-        # neighbours' streams wait on it (no host barrier per period)
-        self._counter = peer.DeviceVector(1, self.device)
-        self._counter.tensor.zero_()
+        # edge counters (osc_edge_sync_t.counters): [0]/[1] our left/right
+        # edge done through period q, [2]/[3] tallies, [4..7] timeout record
+        self._counters = peer.DeviceVector(8, self.device)
+        self._counters.tensor.zero_()
         self._period = 0
         torch.cuda.synchronize(self.device)
         mine = {"blo": self.L.blo, "bufs": [b.handle() for b in self._own],
-                "counter": self._counter.handle()}
+                "counters": self._counters.handle()}
         infos = [None] * self.world
         dist.all_gather_object(infos, mine, group=self.host_group)
         self._imported = []
-        for nb in (self.rank - 1, self.rank + 1):
+        self._ready = [None, None]  # the neighbours' counters facing us
+        for side, nb in enumerate((self.rank - 1, self.rank + 1)):
             if 0 <= nb < self.world:
                 ptrs = [peer.import_buffer(h) for h in infos[nb]["bufs"]]
-                self._imported += ptrs
+                ctr = peer.import_buffer(infos[nb]["counters"])
+                self._imported += ptrs + [ctr]
                 self.peer_bufs[nb] = (((ptrs[0], ptrs[1]), (ptrs[2], ptrs[3])), infos[nb]["blo"])
-                self.peer_counters[nb] = peer.import_buffer(infos[nb]["counter"])
-                self._imported.append(self.peer_counters[nb])
-        # Can this system wait on the mapped counters from a stream?  Try a
-        # wait that is already satisfied; every rank adopts host ordering if
-        # any rank cannot (all ranks must order periods the same way).
-        ok = True
-        try:
-            probe = torch.cuda.current_stream(self.device)
-            for ptr in self.peer_counters.values():
-                peer.stream_wait_u64(probe, ptr, 0)
-                peer.stream_write_u64(probe, self._counter.ptr, 0)
-            torch.cuda.synchronize(self.device)
-        except RuntimeError:
-            ok = False
-        if os.environ.get("OSC_PEER_HOST_ORDER") == "1":  # exercise the fallback
-            ok = False
-        oks = [None] * self.world
-        dist.all_gather_object(oks, ok, group=self.host_group)
-        self._host_order = not all(oks)
+                # the left neighbour's RIGHT edge counter ([1]) and vice versa
+                self._ready[side] = ctr + 8 * (1 - side)
+        self._host_order = os.environ.get("OSC_PEER_HOST_ORDER") == "1"
+        self._phase("peer-ready")
+
+    def _phase(self, name, period=None):
+        """Per-phase host timestamps (kept for the error report; dumped to
+        $OSC_PEER_TRACE/rank<r>.json at close when set)."""
+        self.trace.append((round(time.monotonic() - self._t0, 6), name, period))
 
     def close(self):
         """Release peer resources in a safe order: finish local work, unmap the
@@ -210,13 +261,17 @@ class ShardedChain:
         then free the allocations this rank exported."""
         if not getattr(self, "_own", None):
             return
+        torch.cuda.synchronize(self.device)
+        self._phase("close")
+        dist.barrier(group=self.host_group)  # no rank still writes into anyone
+        self._release_peer()
+
+    def _release_peer(self):
         from . import peer
 
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.host_group)  # no rank still writes into anyone
         for ptr in self._imported:
             peer.close_buffer(ptr)
-        self._imported, self.peer_counters = [], {}
+        self._imported = []
         self.peer_bufs.clear()
         dist.barrier(group=self.host_group)  # every mapping of our memory is gone
         # keep the results readable: move them to ordinary tensors first
@@ -225,8 +280,13 @@ class ShardedChain:
         torch.cuda.synchronize(self.device)
         for b in self._own:
             b.free()
-        self._counter.free()
+        self._counters.free()
         self._own = []
+        path = os.environ.get("OSC_PEER_TRACE")
+        if path:
+            os.makedirs(path, exist_ok=True)
+            with open(os.path.join(path, f"rank{self.rank}.json"), "w") as f:
+                json.dump(self.trace, f)
 
     def __enter__(self):
         return self
@@ -235,52 +295,45 @@ class ShardedChain:
         self.close()
 
     def _run_peer(self, nsteps):
-        """Fused exchange, ordered on the device: before period q (a running
-        count over runs) our stream waits until each neighbour's counter shows
-        its period q-1 done -- it produced our ghosts and finished reading the
-        buffer we now store into (ping-pong) -- and after our launch it stores
-        q + 1 into our counter.  The waits happen in the GPU front-end; no
-        kernel ever spins on another GPU and no host barrier is needed."""
-        from . import peer
-
-        main = torch.cuda.current_stream(self.device)
+        """Fused exchange, one launch per period, ordered on the device: each
+        launch's edge tiles wait (bounded) for the neighbours' edge counters
+        to reach the global period q (a running count over runs, so the
+        ping-pong parity carries across runs) and post ours when done.  With
+        OSC_PEER_HOST_ORDER=1 the periods are ordered on the host instead
+        (finish, host barrier): slower, same bytes."""
         a, b = self.L.own
         k = 0
+        self._phase("run", self._period)
         while k < nsteps:
             n = min(self.T, nsteps - k)
             q = self._period
-            self._order_before(main, q)
             left, right = self.peer_descriptors(q)
+            sync = None
+            if not self._host_order:
+                sync = (self._ready[0], self._ready[1], self._counters.ptr, q, self.timeout_ns)
             self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, k,
-                         self.first_bad, left=left, right=right)
-            self._order_after(main, q)
+                         self.first_bad, left=left, right=right, sync=sync)
+            if self._host_order:
+                torch.cuda.synchronize(self.device)  # our period (and its peer stores) done
+                dist.barrier(group=self.host_group)
             self.x, self.x2 = self.x2, self.x
             self.v, self.v2 = self.v2, self.v
             self._period += 1
             k += n
-        # neighbours' final writes land only in ghost zones; our owned cells are
-        # complete on our stream.  Make sure no peer kernel still targets us.
-        self._order_before(main, self._period)
+        self._phase("enqueued", self._period)
+        self._check_sync()
 
-    # Period ordering: stream counters when every rank's system takes stream
-    # memory operations on the mapped counters (decided together at setup),
-    # else host ordering -- finish our period, then a host barrier: slower,
-    # equally correct.
-    def _order_before(self, main, q):
+    def _check_sync(self):
+        """Finish our launches and read the timeout record: a wait that
+        expired raises PeerTimeoutError here, before any collective (a stuck
+        neighbour could not join one)."""
         from . import peer
 
-        if not self._host_order:
-            for ptr in self.peer_counters.values():
-                peer.stream_wait_u64(main, ptr, q)
-
-    def _order_after(self, main, q):
-        from . import peer
-
-        if self._host_order:
-            torch.cuda.synchronize(self.device)  # our period (and its peer stores) done
-            dist.barrier(group=self.host_group)
-        else:
-            peer.stream_write_u64(main, self._counter.ptr, q + 1)
+        rec = peer.edge_sync_status(self._counters.ptr, torch.cuda.current_stream(self.device))
+        self._phase("synced", self._period)
+        if rec is not None:
+            period, side, seen = rec
+            raise PeerTimeoutError(self.rank, period, side, seen, list(self.trace))
 
     # -- ghost exchange ------------------------------------------------------
     def boundary(self, x, v):

@@ -62,7 +62,7 @@ def test_argument_errors_need_no_device(lib):
                               None, 0x80, None) == _native.OSC_INVALID
     assert b"flags" in lib.osc_last_error()
     assert lib.osc_rk4_chain_advance(None, None, None, None, None, None, 100, 0, 100, 1e-3, 600,
-                                     0, None, None, None, 0, None) == _native.OSC_INVALID
+                                     0, None, None, None, None, 0, None) == _native.OSC_INVALID
     # validation entry points (modal.py): compare of an empty trajectory is
     # the reference's ValueError("empty trajectory") (modal.py:143-144)
     assert lib.osc_compare_batch2(None, None, None, 0, 4, None, None) == _native.OSC_INVALID

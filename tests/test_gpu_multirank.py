@@ -1,7 +1,9 @@
-"""Two real processes sharding one chain on the CUDA kernel (gloo transport,
-both ranks on cuda:0 -- the kernels of the two ranks never wait on each
-other; the host-driven exchange is the only coupling).  Byte-identical to
-the single-GPU integration."""
+"""Two and three real processes sharding one chain on the CUDA kernel (gloo
+process group, every rank on cuda:0).  Byte-identical to the single-GPU
+integration.  With the fused peer transport the ranks' kernels order their
+edge tiles on the device with bounded waits; on one GPU the processes'
+contexts are time-sliced, so a waiting CTA never blocks its neighbour's
+progress -- and a neighbour that stops raises PeerTimeoutError."""
 
 import os
 import socket
@@ -148,3 +150,50 @@ def test_peer_transport_host_ordering_fallback(monkeypatch):
     ref = batched.integrate_chains(*_chain(s, 21), 1e-3, sum(runs))
     assert fb == 0
     assert bits(x) == bits(ref.x[0].cpu().numpy()) and bits(v) == bits(ref.v[0].cpu().numpy())
+
+
+def _worker_stuck(rank, world, port, s, T, stuck, timeout_ms, q):
+    """Rank `stuck` maps its buffers and counters but never runs a period;
+    the others must get PeerTimeoutError instead of hanging."""
+    import time
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1702_02207_b200 import sharded
+
+        sh = sharded.ShardedChain(*_chain(s, 21), 1e-3, halo_steps=T, transport="peer",
+                                  timeout_ms=timeout_ms)
+        out = None
+        if rank != stuck:
+            t0 = time.monotonic()
+            try:
+                sh.run(6 * T)
+                out = ("no error", None)
+            except sharded.PeerTimeoutError as exc:
+                out = ((exc.rank, exc.period, exc.side, exc.seen), time.monotonic() - t0)
+        results = [None] * world
+        dist.all_gather_object(results, out)
+        sh.close()
+        if rank == 0:
+            q.put(results)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,stuck", [(2, 1), (3, 1)])
+def test_stuck_neighbour_raises_instead_of_hanging(world, stuck):
+    """The fused exchange's waits are bounded (osc_edge_sync_t.timeout_ns):
+    a neighbour that never posts its edge counter makes every adjacent rank
+    raise PeerTimeoutError naming itself, the period (1: period 0 needs only
+    the initial state), the side and the counter value seen (0)."""
+    results = collect(_worker_stuck, (world, _port(), 60_000, 8, stuck, 300.0), world)
+    for rank, out in enumerate(results):
+        if rank == stuck:
+            assert out is None
+            continue
+        (r, period, side, seen), elapsed = out
+        assert r == rank and period == 1 and seen == 0
+        assert side == (1 if rank < stuck else 0)
+        assert elapsed < 20.0  # one timeout, then the launches drain

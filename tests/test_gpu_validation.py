@@ -135,7 +135,7 @@ def test_other_entry_points_reject():
             _p(md), _p(Cd), _p(xd), _p(vd), s, 1e-4, 10, 10, None, None, _p(fb), _p(ns), st),
         "osc_rk4_chain_advance": lambda: lib.osc_rk4_chain_advance(
             _p(md), _p(Cd), _p(xd), _p(vd), _p(out), _p(out), s, 0, s, 1e-4, 4, 0, _p(fb), None,
-            None, 0, st),
+            None, None, 0, st),
         "osc_rk4_chains": lambda: lib.osc_rk4_chains(
             _p(md), _p(Cd), _p(xd.clone()), _p(vd.clone()), 1, s, 1e-4, 10, 10, None, None, None,
             _p(fb), 0, 0, st),

@@ -204,6 +204,33 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           const osc_peer_t *right, const osc_edge_sync_t *sync, uint32_t flags,
                           void *stream);
 
+/* One shard of a chain in the multi-process fused exchange (one process per
+ * GPU): the period loop of osc_rk4_chain_advance launches in native code, so
+ * a run of P periods costs P kernel launches of host time and nothing else.
+ * Period q (sync.period, counted over all runs) reads our buffer q % 2,
+ * writes our owned cells into buffer (q + 1) % 2 and our first / last `ghost`
+ * owned cells into the left / right neighbour's buffer (q + 1) % 2 at cell
+ * c + offset[side]; its edge tiles are ordered with the neighbours on the
+ * device (osc_edge_sync_t).  x[b], v[b]: our buffer b (n cells, ghosts
+ * included); nx[side][b], nv[side][b]: the neighbour's buffer b, mapped peer
+ * memory (NULL for a chain end).  On return sync.period has advanced by the
+ * number of periods enqueued; the state is in buffer sync.period % 2.
+ * Asynchronous (stream-ordered); parameters are not re-validated (validate
+ * the shard once: osc_validate_parameters).  first_bad: [1] device. */
+typedef struct {
+    const double *m, *C;
+    double *x[2], *v[2];
+    double *nx[2][2], *nv[2][2];
+    int64_t n, own_lo, own_hi;
+    int64_t offset[2];
+    int64_t ghost;
+    int64_t *first_bad;
+    osc_edge_sync_t sync;
+} osc_shard_t;
+
+int osc_rk4_shard_run(osc_shard_t *shard, double dt, int64_t nsteps, int64_t halo_steps,
+                      int64_t step0, uint32_t flags, void *stream);
+
 /* Stream-ordered 64-bit counters, for ordering work across processes
  * without host synchronisation: osc_stream_write_u64 stores value at addr
  * once all prior work of stream is done (preceded by a system-scope fence, so

@@ -44,6 +44,7 @@ SIGNATURES = {
                                              _dbl, _i64, _i64, _vp, _vp, _vp, _vp,
                                              ctypes.c_uint32, _vp]),
     "osc_edge_sync_status": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_uint64), _vp]),
+    "osc_rk4_shard_run": (ctypes.c_int, [_vp, _dbl, _i64, _i64, _i64, ctypes.c_uint32, _vp]),
     "osc_stream_write_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_stream_wait_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_chain_plan": (ctypes.c_int, [_i64, _i64, _i64, _i64, _vp]),
@@ -93,6 +94,17 @@ class EdgeSync(ctypes.Structure):
 
     _fields_ = [("ready", ctypes.c_void_p * 2), ("counters", ctypes.c_void_p),
                 ("period", ctypes.c_uint64), ("timeout_ns", ctypes.c_int64)]
+
+
+class Shard(ctypes.Structure):
+    """osc_shard_t: one shard of the multi-process fused exchange."""
+
+    _fields_ = [("m", ctypes.c_void_p), ("C", ctypes.c_void_p),
+                ("x", ctypes.c_void_p * 2), ("v", ctypes.c_void_p * 2),
+                ("nx", (ctypes.c_void_p * 2) * 2), ("nv", (ctypes.c_void_p * 2) * 2),
+                ("n", ctypes.c_int64), ("own_lo", ctypes.c_int64), ("own_hi", ctypes.c_int64),
+                ("offset", ctypes.c_int64 * 2), ("ghost", ctypes.c_int64),
+                ("first_bad", ctypes.c_void_p), ("sync", EdgeSync)]
 
 
 class NativeUnavailableError(RuntimeError):

@@ -154,6 +154,40 @@ int osc_stream_wait_u64(void *stream, const void *addr, uint64_t value)
 }
 
 // ---------------------------------------------------------------------------
+// One shard's period loop of the multi-process fused exchange.
+// ---------------------------------------------------------------------------
+int osc_rk4_shard_run(osc_shard_t *sh, double dt, int64_t nsteps, int64_t halo_steps,
+                      int64_t step0, uint32_t flags, void *stream)
+{
+    if (!sh)
+        return fail(OSC_INVALID, "null shard");
+    if (int rc = check_run_args(dt, nsteps, 1))
+        return rc;
+    if (halo_steps < 1 || sh->ghost < 0)
+        return fail(OSC_INVALID, "halo_steps must be >= 1");
+    const int64_t T = halo_steps;
+    for (int64_t k = 0; k < nsteps;) {
+        const int64_t n = std::min(T, nsteps - k);
+        const int b = static_cast<int>(sh->sync.period & 1), nb = b ^ 1;
+        osc_peer_t peer[2] = {};
+        for (int side = 0; side < 2; ++side)
+            if (sh->nx[side][nb])
+                peer[side] = osc_peer_t{sh->nx[side][nb], sh->nv[side][nb], sh->offset[side],
+                                        sh->ghost};
+        if (int rc = osc_rk4_chain_advance(sh->m, sh->C, sh->x[b], sh->v[b], sh->x[nb],
+                                           sh->v[nb], sh->n, sh->own_lo, sh->own_hi, dt, n,
+                                           step0 + k, sh->first_bad,
+                                           peer[0].x ? &peer[0] : nullptr,
+                                           peer[1].x ? &peer[1] : nullptr, &sh->sync,
+                                           flags | OSC_TRUSTED, stream))
+            return rc;
+        ++sh->sync.period;
+        k += n;
+    }
+    return OSC_OK;
+}
+
+// ---------------------------------------------------------------------------
 // One chain sharded over the GPUs of this process, fused halo exchange.
 // ---------------------------------------------------------------------------
 namespace {

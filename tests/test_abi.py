@@ -172,3 +172,36 @@ def test_chain_launch_plan(lib):
         (8, 128, 512, 20)
     with pytest.raises(ValueError):
         batched.chain_plan(1, 1 << 20, 100, halo_steps=600)
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of osc_peer_t / osc_edge_sync_t / osc_shard_t have
+    the C layout (sizes and field offsets from a compiled probe)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:  # pragma: no cover
+        pytest.skip("no C compiler")
+    src = tmp_path / "probe.c"
+    src.write_text('''
+#include <stddef.h>
+#include <stdio.h>
+#include "osc_b200.h"
+int main(void) {
+    printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(osc_peer_t), sizeof(osc_edge_sync_t),
+           sizeof(osc_shard_t), offsetof(osc_shard_t, nx), offsetof(osc_shard_t, n),
+           offsetof(osc_shard_t, ghost), offsetof(osc_shard_t, first_bad),
+           offsetof(osc_shard_t, sync));
+    return 0;
+}
+''')
+    exe = tmp_path / "probe"
+    subprocess.run([gcc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(t) for t in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    S = _native.Shard
+    want = [ctypes.sizeof(_native.Peer), ctypes.sizeof(_native.EdgeSync), ctypes.sizeof(S),
+            S.nx.offset, S.n.offset, S.ghost.offset, S.first_bad.offset, S.sync.offset]
+    assert got == want

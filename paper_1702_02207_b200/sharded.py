@@ -248,6 +248,8 @@ class ShardedChain:
                 # the left neighbour's RIGHT edge counter ([1]) and vice versa
                 self._ready[side] = ctr + 8 * (1 - side)
         self._host_order = os.environ.get("OSC_PEER_HOST_ORDER") == "1"
+        self._shard_desc = None
+        self.host_s_per_period = None
         self._phase("peer-ready")
 
     def _phase(self, name, period=None):
@@ -304,6 +306,12 @@ class ShardedChain:
         a, b = self.L.own
         k = 0
         self._phase("run", self._period)
+        if not self._host_order and self.advance is _cuda_advance:
+            # the whole period loop in native code (osc_rk4_shard_run)
+            t = time.perf_counter()
+            periods = self._native_run(nsteps)
+            self.host_s_per_period = (time.perf_counter() - t) / max(periods, 1)
+            k = nsteps
         while k < nsteps:
             n = min(self.T, nsteps - k)
             q = self._period
@@ -322,6 +330,54 @@ class ShardedChain:
             k += n
         self._phase("enqueued", self._period)
         self._check_sync()
+
+    def _native_run(self, nsteps) -> int:
+        """Enqueue every period of this run with one C call; returns the
+        number of periods.  Buffer b of ours is (x, v) when the global
+        period is even, (x2, v2) when odd -- the parity the Python loop
+        keeps by swapping."""
+        import ctypes
+
+        from . import _native
+
+        lib = _native.lib()
+        own = self._own  # buffer 0 = _own[0:2], buffer 1 = _own[2:4]
+        sh = self._shard_desc
+        if sh is None:
+            sh = self._shard_desc = _native.Shard()
+            sh.m, sh.C = self.m.data_ptr(), self.C.data_ptr()
+            for bidx in range(2):
+                sh.x[bidx], sh.v[bidx] = own[2 * bidx].ptr, own[2 * bidx + 1].ptr
+            for side, nb in enumerate((self.rank - 1, self.rank + 1)):
+                if nb in self.peer_bufs:
+                    bufs, nblo = self.peer_bufs[nb]
+                    for bidx in range(2):
+                        sh.nx[side][bidx], sh.nv[side][bidx] = bufs[bidx]
+                    sh.offset[side] = self.L.blo - nblo
+            sh.n = self.L.n
+            sh.own_lo, sh.own_hi = self.L.own
+            sh.ghost = self.L.g
+            sh.first_bad = self.first_bad.data_ptr()
+            sh.sync.ready[0] = self._ready[0]
+            sh.sync.ready[1] = self._ready[1]
+            sh.sync.counters = self._counters.ptr
+            sh.sync.timeout_ns = self.timeout_ns
+        sh.sync.period = self._period
+        # the state must be in buffer period % 2 (the Python loop's swaps keep
+        # self.x on the current buffer; the native loop relies on parity)
+        cur = own[2 * (self._period % 2)].ptr
+        assert self.x.data_ptr() == cur, "shard state is not in buffer period % 2"
+        rc = lib.osc_rk4_shard_run(ctypes.byref(sh), self.dt, int(nsteps), self.T, 0, 0,
+                                   ctypes.c_void_p(torch.cuda.current_stream(self.device)
+                                                   .cuda_stream))
+        if rc != _native.OSC_OK:
+            raise RuntimeError(f"osc_rk4_shard_run: {_native.last_error()}")
+        periods = int(sh.sync.period) - self._period
+        if periods % 2:
+            self.x, self.x2 = self.x2, self.x
+            self.v, self.v2 = self.v2, self.v
+        self._period = int(sh.sync.period)
+        return periods
 
     def _check_sync(self):
         """Finish our launches and read the timeout record: a wait that

@@ -59,6 +59,8 @@ def _worker(rank, world, port, seed, runs, q):
             fb = sh.run(nsteps)
             x, v = sh.gather()
             rec["trace"] = sh.trace[-4:]
+            rec["host_us_per_period"] = (None if sh.host_s_per_period is None
+                                         else round(sh.host_s_per_period * 1e6, 2))
             sh.close()
             rec["seconds"] = round(time.monotonic() - t0, 4)
             if rank == 0:
@@ -96,6 +98,7 @@ def main():
     ctx = mp.get_context("spawn")
     total = ok = bad = hung = 0
     worst = 0.0
+    host_us = []
     t_start = time.monotonic()
     for gidx in range(args.groups):
         world = 2 + gidx % 2
@@ -131,6 +134,8 @@ def main():
             ok += bool(rec.get("ok"))
             bad += not rec.get("ok")
             worst = max(worst, rec.get("seconds", 0.0))
+            if rec.get("host_us_per_period") is not None:
+                host_us.append(rec["host_us_per_period"])
             lines.write(json.dumps(rec) + "\n")
             lines.flush()
         try:
@@ -141,7 +146,9 @@ def main():
     lines.close()
     summary = (f"peer transport soak: {total} runs ({args.groups} process groups of 2/3 ranks, "
                f"{args.runs} runs each) -> {ok} byte-exact, {bad} failed, {hung} hung groups; "
-               f"slowest run {worst:.2f} s; wall {time.monotonic() - t_start:.0f} s")
+               f"slowest run {worst:.2f} s; host time per period (native loop) median "
+               f"{(sorted(host_us)[len(host_us) // 2] if host_us else float('nan')):.1f} us; "
+               f"wall {time.monotonic() - t_start:.0f} s")
     print(summary)
     with open(args.out + ".txt", "w") as f:
         f.write(summary + "\n")

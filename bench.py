@@ -6,9 +6,12 @@ systems, fp64, dt=1e-4, 10^4 RK4 steps, seeded synthetic inputs.  One bench
 Metric: DOF-steps/s (whole job, all ranks).  --config C1/C3/C4 times the other
 single-GPU configurations the same way (DESIGN.md lists their lines).
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): C2/C4 are independent systems,
-so every rank integrates its own seeded batch of the full per-GPU size (weak
-scaling, no data-path collective); device time is the max over ranks.
+Multi-GPU (torchrun, one rank per GPU, NCCL): the ranks split the ONE
+workload (strong scaling) -- C2 systems, C4 chains and C5
+trajectory columns in contiguous slices with no data-path collective, C3 as
+a 1-D domain decomposition with a ghost exchange every T steps; device time
+is the max over ranks.  At N > 1 the default line also carries `sharded_c3`:
+C3 over the same N ranks through the fused peer exchange.
 
 --impl reference times the reference algorithm on the host CPU (the
 byte-identical C restatement in oracle/, all host threads) on a bounded sample
@@ -164,12 +167,15 @@ class ClockSampler:
 
 def workload_desc(name: str, world: int = 1, transport: str = "nccl", T=None) -> dict:
     """The `config` description of a workload (shared by both bench arms)."""
+    split = "one seeded draw split into G contiguous slices, one per rank (no collective)"
     if name == "C2":
         return {"workload": "C2: 2^20 independent 2-DOF systems (eq. 2), SoA [2][B]",
-                "systems_per_gpu": workloads.C2_B}
+                "systems": workloads.C2_B, "systems_per_gpu": workloads.C2_B // world,
+                "sharding": split}
     if name == "C4":
         return {"workload": "C4: 4096 chains x 1024 cells, [B][s]",
-                "chains_per_gpu": workloads.C4_B, "cells_per_chain": workloads.C4_S}
+                "chains": workloads.C4_B, "chains_per_gpu": workloads.C4_B // world,
+                "cells_per_chain": workloads.C4_S, "sharding": split}
     if name == "C3":
         return {"workload": "C3: one wall-anchored chain of 2^24 cells",
                 "cells": workloads.C3_S, "halo_steps": T,
@@ -177,11 +183,57 @@ def workload_desc(name: str, world: int = 1, transport: str = "nccl", T=None) ->
                             f"refreshed every T steps ({transport})"}
     if name == "C5":
         return {"workload": "C5: dense SPD system s=4096, A = M^-1 K, 1024 trajectories",
-                "s": workloads.C5_S, "trajectories_per_gpu": workloads.C5_N,
+                "s": workloads.C5_S, "trajectories": workloads.C5_N,
+                "trajectories_per_gpu": workloads.C5_N // world,
+                "sharding": "M, K built once on rank 0 and broadcast; trajectory columns "
+                            "split G ways (no collective per step)",
                 "gemm_per_launch": "4096 x 4096 x 2048 fp64 (DMMA), RK4 epilogue fused"}
     if name == "C1":
         return {"workload": "C1: paper 2-DOF system, C/m=1012.5, 10^6 steps (latency)"}
     raise SystemExit(f"unknown config {name}")
+
+
+# implementation details of a workload description, kept out of `config` so
+# that both bench arms report the identical workload configuration
+IMPL_KEYS = ("halo_steps", "sharding", "gemm_per_launch")
+
+
+def shared_config(name: str, world: int) -> dict:
+    """The workload configuration both arms report (identical by construction):
+    sizes, dt, steps per bench step, the whole job's DOF-steps and how the N
+    GPUs split it."""
+    p = workloads.PARAMS[name]
+    desc = {k: v for k, v in workload_desc(name, world).items() if k not in IMPL_KEYS}
+    total = {"C1": 2 * world, "C2": 2 * workloads.C2_B, "C3": workloads.C3_S,
+             "C4": workloads.C4_B * workloads.C4_S,
+             "C5": workloads.C5_S * workloads.C5_N}[name]
+    return dict(desc, dt=p.dt, nsteps_per_step=p.nsteps, dof_steps_per_step=total * p.nsteps,
+                parallelism={"C1": f"replicas{world}",
+                             "C3": f"shards{world}"}.get(name, f"dp{world}"))
+
+
+def c5_broadcast(rank, world, device):
+    """workloads.c5() built once, on rank 0, and broadcast ("A
+    built per GPU from the seed or broadcast once" -- the 4096^2 QR is the
+    expensive part).  Host arrays on every rank."""
+    if world == 1:
+        return workloads.c5()
+    import torch
+    import torch.distributed as dist
+
+    s, N = workloads.C5_S, workloads.C5_N
+    shapes = ((s,), (s, s), (s, N), (s, N))
+    host = workloads.c5() if rank == 0 else None
+    out = []
+    nccl = dist.get_backend() == "nccl"
+    for i, shape in enumerate(shapes):
+        t = (torch.from_numpy(host[i]) if rank == 0
+             else torch.empty(shape, dtype=torch.float64))
+        if nccl:
+            t = t.to(device)
+        dist.broadcast(t, src=0)
+        out.append(t.cpu().numpy())
+    return tuple(out)
 
 
 class Workload:
@@ -194,17 +246,27 @@ class Workload:
         p = workloads.PARAMS[name]
         self.dt, self.nsteps = p.dt, p.nsteps
         self.halo = halo
+        self.world = world
         if name == "C2":
-            arrays = workloads.c2(rank=rank)
+            # strong split: rank r integrates systems
+            # [rB/G, (r+1)B/G) of the one seeded draw; no collective
+            arrays = workloads.c2()
+            self.total_dof = arrays[0].size
+            sl = workloads.part(workloads.C2_B, rank, world)
+            arrays = tuple(np.ascontiguousarray(a[:, sl]) for a in arrays)
             self.kernel, self.launches = "batch2_rk4_kernel", 1
-            self.desc = workload_desc(name)
+            self.desc = workload_desc(name, world)
         elif name == "C4":
-            arrays = workloads.c4(rank=rank)
+            arrays = workloads.c4()
+            self.total_dof = arrays[0].size
+            sl = workloads.part(workloads.C4_B, rank, world)
+            arrays = tuple(np.ascontiguousarray(a[sl]) for a in arrays)
             self.kernel = "chain_rk4_kernel<8>"
             self.launches = -(-p.nsteps // 512)
-            self.desc = workload_desc(name)
+            self.desc = workload_desc(name, world)
         elif name == "C3":
             arrays = workloads.c3()
+            self.total_dof = arrays[0].size
             plan = batched.chain_plan(1, workloads.C3_S, p.nsteps, halo)
             T = plan["steps_per_launch"]
             self.kernel = "chain_tiles_persistent<8,256>"
@@ -215,13 +277,19 @@ class Workload:
             if world > 1 and transport == "nccl":
                 self.launches = 3 * self.launches  # interior + 2 edge launches per period
         elif name == "C5":
-            arrays = workloads.c5(rank=rank)  # m, K, X0, V0
+            # m, K built ONCE (rank 0: the QR of a 4096^2 draw) and broadcast;
+            # rank r integrates trajectory columns [rN/G, (r+1)N/G)
+            arrays = c5_broadcast(rank, world, device)  # m, K, X0, V0
+            self.total_dof = arrays[2].size
+            sl = workloads.part(workloads.C5_N, rank, world)
+            arrays = arrays[:2] + tuple(np.ascontiguousarray(a[:, sl]) for a in arrays[2:])
             self.kernel = "dense_rk4_gemm"
             self.launches = 2 * p.nsteps  # + rowscale, pack, unpack (counted in gpu_launches)
-            self.desc = workload_desc(name)
+            self.desc = workload_desc(name, world)
         elif name == "C1":
             arrays = workloads.c1()
             arrays = tuple(a[:, None] for a in arrays)
+            self.total_dof = 2 * world  # replicas
             self.kernel, self.launches = "batch2_rk4_kernel", 1
             self.desc = workload_desc(name)
         else:
@@ -242,6 +310,7 @@ class Workload:
             self.shard_v0 = self.shard.v.clone()
             self.dof = hi - lo
         self.dof_steps = self.dof * self.nsteps
+        self.total_dof_steps = self.total_dof * self.nsteps
 
     def step(self):
         m, C, x0, v0 = self.dev
@@ -534,14 +603,13 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-        "higher_is_better": True, "scaling": "strong" if wl_name == "C3" else "weak",
+        "higher_is_better": True, "scaling": "weak" if wl_name == "C1" else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy PCG64, workloads.py)",
-        "config": dict({k: v for k, v in workload_desc(wl_name).items()
-                        if k not in ("halo_steps", "sharding", "gemm_per_launch")}, dt=wl.dt,
-                       nsteps_per_step=wl.nsteps, parallelism=f"{last['cores']} host threads",
-                       arithmetic="IEEE fp64 CPU restatement, byte-identical to "
-                                  "oscbench.integrate"),
+        "config": shared_config(wl_name, world),
+        "impl_notes": {"execution": f"{last['cores']} host threads (rank 0 only)",
+                       "arithmetic": "IEEE fp64 CPU restatement, byte-identical to "
+                                     "oscbench.integrate"},
         "cpu_baseline": dict(last, value=value),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -640,7 +708,7 @@ def main():
         n_e2e = max(1, min(args.steps, 5))
         if world > 1:
             e2e_s = allreduce_max(e2e_s, device, backend)
-        e2e = {"value": world * wl.dof_steps * n_e2e / e2e_s, "unit": UNIT,
+        e2e = {"value": wl.total_dof_steps * n_e2e / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "timing": "wall clock around the synchronous host-pointer C-ABI call "
                          "(pinned host buffers; H2D + kernels + D2H inside)"}
@@ -703,7 +771,9 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    value = world * wl.dof_steps * args.steps / dev_s
+    # whole-job throughput: every rank's DOF-steps (the ranks partition the
+    # one workload, C1 replicas aside) over the slowest rank's device time
+    value = wl.total_dof_steps * args.steps / dev_s
     per_gpu = wl.dof_steps * args.steps / dev_s
     launch_s = dev_s / (args.steps * wl.launches)
     hbm_peak, hbm_src = peaks()
@@ -747,18 +817,17 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "strong" if wl.name == "C3" else "weak",
+        "higher_is_better": True, "scaling": "weak" if wl.name == "C1" else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy PCG64, workloads.py; no dataset exists)",
-        "config": dict(wl.desc, dt=wl.dt, nsteps_per_step=wl.nsteps,
-                       dof_steps_per_gpu_step=wl.dof_steps,
-                       parallelism={"C1": f"replicas{world}",
-                                    "C3": f"shards{world}"}.get(wl.name, f"dp{world}"),
-                       l2="flushed between timed steps (256 MiB memset outside step events); "
-                          "state is register-resident within a step",
-                       arithmetic=("IEEE fp64; GEMM summation order differs from CPU BLAS "
-                                   "(rel. 1e-10 vs the restatement)" if wl.name == "C5" else
-                                   "IEEE fp64, byte-identical to oscbench.integrate")),
+        "config": shared_config(wl.name, world),
+        "impl_notes": dict({k: v for k, v in wl.desc.items() if k in IMPL_KEYS},
+                           dof_steps_per_gpu_step=wl.dof_steps,
+                           l2="flushed between timed steps (256 MiB memset outside step "
+                              "events); state is register-resident within a step",
+                           arithmetic=("IEEE fp64; GEMM summation order differs from CPU BLAS "
+                                       "(rel. 1e-10 vs the restatement)" if wl.name == "C5"
+                                       else "IEEE fp64, byte-identical to oscbench.integrate")),
         "roofline": roofline,
         "roofline_fp64": {
             "bound": "fp64_pipe", "dp_inst_per_dof_step": dp, "dp_count_source": dp_src,

@@ -45,10 +45,16 @@ PARAMS = {
 }
 
 
-def _rng(rank: int = 0):
-    # rank 0 reproduces the single-GPU configuration exactly; other ranks of a
-    # weak-scaling run draw their own independent systems.
-    return np.random.default_rng(SEED if rank == 0 else [SEED, rank])
+def _rng():
+    return np.random.default_rng(SEED)
+
+
+def part(n: int, rank: int, world: int) -> slice:
+    """Rank's contiguous share [n*rank//world, n*(rank+1)//world) of n
+    independent units (C2 systems, C4 chains, C5 trajectory
+    columns) -- a split of the ONE seeded draw, so the union over ranks is
+    exactly the single-GPU workload (strong scaling)."""
+    return slice(n * rank // world, n * (rank + 1) // world)
 
 
 def c1():
@@ -57,9 +63,9 @@ def c1():
             np.array([1.0, 0.0]), np.array([0.0, 0.0]))
 
 
-def c2(B: int = C2_B, rank: int = 0):
+def c2(B: int = C2_B):
     """[2][B]: m ~ U[0.5,2], C ~ U[500,2000], x0 ~ N(0,1), v0 = 0."""
-    rng = _rng(rank)
+    rng = _rng()
     m = rng.uniform(0.5, 2.0, (2, B))
     C = rng.uniform(500.0, 2000.0, (2, B))
     x0 = rng.standard_normal((2, B))
@@ -75,21 +81,21 @@ def c3(s: int = C3_S):
     return m, C, x0, np.zeros(s)
 
 
-def c4(B: int = C4_B, s: int = C4_S, rank: int = 0):
+def c4(B: int = C4_B, s: int = C4_S):
     """[B][s] batch of chains: same distributions as C2."""
-    rng = _rng(rank)
+    rng = _rng()
     m = rng.uniform(0.5, 2.0, (B, s))
     C = rng.uniform(500.0, 2000.0, (B, s))
     x0 = rng.standard_normal((B, s))
     return m, C, x0, np.zeros((B, s))
 
 
-def c5(s: int = C5_S, N: int = C5_N, rank: int = 0):
+def c5(s: int = C5_S, N: int = C5_N):
     """Dense SPD system: M = diag(U[0.5,2]), K = Q diag(U[500,2000]) Q^T.
 
     Returns ``m [s]``, ``K [s][s]`` (symmetrised), ``X0 [s][N]``, ``V0 = 0``.
     """
-    rng = _rng(rank)
+    rng = _rng()
     m = rng.uniform(0.5, 2.0, s)
     c = rng.uniform(500.0, 2000.0, s)
     Q, R = np.linalg.qr(rng.standard_normal((s, s)))

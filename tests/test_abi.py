@@ -152,8 +152,10 @@ def test_workloads_are_seeded():
     m, C, x0, v0 = a
     assert m.shape == (2, 1000) and (m >= 0.5).all() and (m < 2).all()
     assert (C >= 500).all() and (C < 2000).all() and not v0.any()
-    r1 = workloads.c2(B=1000, rank=1)
-    assert not np.array_equal(r1[0], m)
+    # the multi-GPU split is a partition of the one draw (strong scaling)
+    parts = [workloads.part(1000, r, 3) for r in range(3)]
+    assert np.array_equal(np.concatenate([m[:, p] for p in parts], axis=1), m)
+    assert [p.stop - p.start for p in parts] == [333, 333, 334]
     m, C, x0, v0 = workloads.c1()
     assert (C / m == 1012.5).all()
 

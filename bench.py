@@ -267,7 +267,9 @@ class Workload:
         elif name == "C3":
             arrays = workloads.c3()
             self.total_dof = arrays[0].size
-            plan = batched.chain_plan(1, workloads.C3_S, p.nsteps, halo)
+            # T per shard: the plan for the (largest) shard's owned cells, the
+            # same on every rank (neighbours must agree on the ghost width)
+            plan = batched.chain_plan(1, -(-workloads.C3_S // world), p.nsteps, halo)
             T = plan["steps_per_launch"]
             self.kernel = "chain_tiles_persistent<8,256>"
             self.launches = plan["launches"]
@@ -437,6 +439,122 @@ class Workload:
             if i >= warmup:
                 times.append(dt)
         return sum(times), h2d, d2h
+
+
+def python_reference_baseline(name, host, dt, nsteps, budget_s=8.0):
+    """The reference's OWN CPU path, timed: ``oscbench.integrate`` (the
+    unmodified package installed in baseline/_ref) under a
+    multiprocessing.Pool of all host cores, each process integrating distinct
+    systems / chains of this workload (BASELINE.md's plan).  A
+    bounded sample (about budget_s of wall time), reported as completed
+    DOF-steps per second.  C3 is one chain: the reference integrates it on
+    one core (its thread engine is slower); C5 has no reference path."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "oscbench", "__init__.py")):
+        return {"unavailable": "baseline/_ref missing (scripts/install_reference.sh)"}
+    if name == "C5":
+        return {"unavailable": "the reference has no dense path (SPEC.md:8,188)"}
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    m, C, x0, v0 = host
+    if name in ("C1", "C2"):
+        units = [(m[:, b], C[:, b], x0[:, b], v0[:, b]) for b in range(min(m.shape[1], 100_000))]
+        dof, steps = 2, nsteps
+    elif name == "C4":
+        units = [(m[b], C[b], x0[b], v0[b]) for b in range(m.shape[0])]
+        dof, steps = m.shape[1], nsteps
+    else:  # C3: a 2^16-cell prefix of the chain, one core
+        k = 1 << 16
+        units = [(m[:k], C[:k], x0[:k], v0[:k])]
+        dof, steps, cores = k, nsteps, 1
+    # calibrate the per-step cost on one unit, then size the sample
+    _ref_integrate((ref, units[0], dt, 2))  # imports
+    t = time.perf_counter()
+    _ref_integrate((ref, units[0], dt, 50))
+    per_step = (time.perf_counter() - t) / 50
+    steps = int(max(1, min(steps, budget_s / per_step / 2)))  # >= 2 units per core
+    n_units = int(max(1, min(len(units), cores * budget_s / (per_step * steps))))
+    cores = min(cores, n_units)
+    jobs = [(ref, u, dt, steps) for u in units[:n_units]]
+    ctx = mp.get_context("fork")
+    t = time.perf_counter()
+    if cores > 1:
+        with ctx.Pool(cores) as pool:
+            done = sum(pool.map(_ref_integrate, jobs, chunksize=1))
+    else:
+        done = sum(_ref_integrate(j) for j in jobs)
+    el = time.perf_counter() - t
+    what = {"C1": "systems", "C2": "systems", "C4": "chains", "C3": "chain prefix"}[name]
+    return {"value": done * dof / el, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{n_units} {what} x {steps} of {nsteps} steps, {dof} DOF each; "
+                      f"oscbench.integrate (baseline/_ref, unmodified) in a "
+                      f"multiprocessing.Pool({cores})" if cores > 1 else
+                      f"{n_units} {what} x {steps} of {nsteps} steps, {dof} DOF; "
+                      f"oscbench.integrate on one core"}
+
+
+def _ref_integrate(job):
+    """One unit through the reference's own integrate; returns steps done."""
+    ref, (m, C, x0, v0), dt, steps = job
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import oscbench
+
+    oscbench.integrate(oscbench.build_chain(list(m), list(C)),
+                       oscbench.PhaseState(tuple(x0), tuple(v0)), dt, steps, steps)
+    return steps
+
+
+def sharded_c3_record(rank, world, device, backend, local, steps=2, warmup=2):
+    """C3 over the same N ranks through the fused peer exchange:
+    one 2^24-cell chain in N contiguous shards, ghost zones refreshed by the
+    tile kernels' own peer stores, edge tiles ordered on the device.  Device
+    time per step is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    wl3 = Workload("C3", rank, device, 0, world, transport="peer")
+    for _ in range(warmup):
+        wl3.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    host = []
+    for a, b in ev:
+        a.record()
+        wl3.step()
+        b.record()
+        host.append(wl3.shard.host_s_per_period)
+    torch.cuda.synchronize()
+    dev_s = sum(a.elapsed_time(b) for a, b in ev) * 1e-3
+    dev_s = allreduce_max(dev_s, device, backend)
+    host_us = allreduce_max(max(h or 0.0 for h in host) * 1e6, device, backend)
+    sh = wl3.shard
+    T, g = sh.T, sh.L.g
+    periods = -(-wl3.nsteps // T)
+    per_gpu = wl3.total_dof_steps * steps / dev_s / world
+    fp64 = fp64_peak(local)
+    dp, _ = dp_inst_per_dof_step("C3")
+    sides = 2 if 0 < rank < world - 1 else 1
+    rec = {
+        "value": wl3.total_dof_steps * steps / dev_s, "unit": UNIT, "n_gpus": world,
+        "ms_per_step": dev_s * 1e3 / steps, "steps": steps, "warmup": warmup,
+        "transport": "peer: boundary cells stored by the tile kernel straight into the "
+                     "neighbours' next-input ghost zones (CUDA IPC / NVLink), edge tiles "
+                     "ordered on the device (osc_edge_sync_t), one launch per period",
+        "halo_steps": T, "ghost_cells": g, "periods_per_step": periods,
+        "halo_bytes_per_period": {"per_neighbour": 2 * g * 8, "rank0": 2 * g * 8 * sides},
+        "host_us_per_period_max": host_us,
+        "roofline_fp64": {"bound": "fp64_pipe", "unit": "TFLOP/s",
+                          "achieved": per_gpu * FLOPS_PER_DOF_STEP["C3"] / 1e12,
+                          "peak": fp64 / 1e12,
+                          "frac": per_gpu * FLOPS_PER_DOF_STEP["C3"] / fp64,
+                          "issue_frac": per_gpu * dp / fp64 if dp else None},
+    }
+    sh.close()
+    return rec
 
 
 def cublas_dgemm(device_index):
@@ -611,6 +729,9 @@ def run_reference(args):
                        "arithmetic": "IEEE fp64 CPU restatement, byte-identical to "
                                      "oscbench.integrate"},
         "cpu_baseline": dict(last, value=value),
+        # the reference's own Python integrate on all cores, beside the C port
+        "cpu_baseline_reference": python_reference_baseline(wl_name, wl.host, wl.dt, wl.nsteps,
+                                                            budget_s=budget),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -645,6 +766,8 @@ def main():
                          "fused into the tile kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sharded-c3", action="store_true",
+                    help="at N > 1, skip the sharded C3 sub-record of the default line")
     ap.add_argument("--ref-budget", type=float, default=8.0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -713,9 +836,14 @@ def main():
                "timing": "wall clock around the synchronous host-pointer C-ABI call "
                          "(pinned host buffers; H2D + kernels + D2H inside)"}
 
-    cpu = None
+    cpu = cpu_py = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(wl)
+        cpu_py = python_reference_baseline(wl.name, wl.host, wl.dt, wl.nsteps)
+
+    sharded_c3 = None
+    if world > 1 and args.config == "C2" and not args.no_sharded_c3:
+        sharded_c3 = sharded_c3_record(rank, world, device, backend, local)
 
     fma_line = None
     if wl.name in ("C2", "C3", "C4") and world == 1:
@@ -795,18 +923,6 @@ def main():
                     "DGEMM on the same shape, measured live",
             "cublas_dgemm_tflops": cublas_dgemm(local) / 1e12,
         }
-    else:
-        roofline = {
-            "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak, "traffic": traffic,
-            "kernel": wl.kernel, "launches_per_step": wl.launches,
-            "algorithmic_bytes_per_launch": alg_bytes,
-            "note": f"SURVEY 8d: 48 B per DOF-step (one step per HBM round trip); peak "
-                    f"{hbm_src}.  The kernel keeps state on-chip across steps, so frac > 1 "
-                    f"is expected; its real limit is the FP64 pipe (roofline_fp64).  Launch "
-                    f"duration = device step time / launches_per_step (for C1/C2 it includes "
-                    f"the ~0.3 ms division classify + launch-order partition)",
-        }
     div2_frac = None
     if wl.name in ("C1", "C2") and os.environ.get("OSC_DIV2", "1")[:1] != "0":
         # systems whose two masses admit the two-operation division
@@ -814,6 +930,41 @@ def main():
         div2_frac = float(((cls[0] != 0) & (cls[1] != 0)).double().mean())
     dp, dp_src = dp_inst_per_dof_step(wl.name, div2_frac)
     dp_inst_rate = per_gpu * dp if dp else None
+    # SURVEY 8d's figure: 48 B per DOF-step (one step per HBM round trip);
+    # above 1.0 because the kernels keep the state on-chip for many steps --
+    # kept as a labelled secondary field, not the binding roofline
+    roofline_hbm = {
+        "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        "frac": achieved / hbm_peak, "algorithmic_bytes_per_launch": alg_bytes,
+        "note": f"SURVEY 8d definition (48 B/DOF-step, one step per HBM round trip); peak "
+                f"{hbm_src}.  Not binding: state stays in registers / shared memory across "
+                f"steps, so HBM moves ~{HBM_BYTES_PER_DOF_STEP} B per launch-sized block, "
+                f"not per step (ncu dram bytes: `traffic` of the roofline)",
+    }
+    if wl.name != "C5":
+        flops_launch = FLOPS_PER_DOF_STEP[wl.name] * wl.dof_steps / wl.launches
+        achieved_tf = flops_launch / launch_s / 1e12
+        roofline = {
+            "bound": "fp64_pipe", "achieved": achieved_tf, "peak": fp64 / 1e12,
+            "unit": "TFLOP/s", "frac": achieved_tf * 1e12 / fp64, "traffic": traffic,
+            "kernel": wl.kernel, "launches_per_step": wl.launches,
+            "algorithmic_flops_per_launch": flops_launch,
+            "algorithmic_flops_per_dof_step": FLOPS_PER_DOF_STEP[wl.name],
+            "peak_source": "measured live: osc_bench_fp64 mode 0, independent DFMA chains on "
+                           "every SM (lane-instructions/s; the same pipe issues DADD/DMUL). "
+                           "MEASURED_PEAKS.json has no FP64 entry; profiles/r01/fp64_peaks.json "
+                           "has the DFMA/DADD/DMMA sweep",
+            "peak_note": "1 flop per DP lane-instruction: the bit-exact path cannot contract "
+                         "a*b+c into an FMA (each reference operation rounds separately), so "
+                         "the FMA-doubled 2 flop/inst peak is not reachable by construction",
+            "issue_frac": dp_inst_rate / fp64 if dp_inst_rate else None,
+            "dp_inst_per_dof_step": dp, "dp_count_source": dp_src,
+            "note": "C1 is one serial system (latency-bound, SURVEY 8d): no roofline claim"
+                    if wl.name == "C1" else
+                    "launch duration = device step time / launches_per_step" +
+                    (" (includes the ~0.3 ms division classify + launch-order partition)"
+                     if wl.name == "C2" else ""),
+        }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps,
@@ -829,15 +980,9 @@ def main():
                                        "(rel. 1e-10 vs the restatement)" if wl.name == "C5"
                                        else "IEEE fp64, byte-identical to oscbench.integrate")),
         "roofline": roofline,
-        "roofline_fp64": {
-            "bound": "fp64_pipe", "dp_inst_per_dof_step": dp, "dp_count_source": dp_src,
-            "achieved_dp_inst_per_s": dp_inst_rate, "peak_dp_inst_per_s": fp64,
-            "frac": dp_inst_rate / fp64 if dp_inst_rate else None,
-            "algorithmic_flops_per_dof_step": FLOPS_PER_DOF_STEP[wl.name],
-            "achieved_flops": per_gpu * FLOPS_PER_DOF_STEP[wl.name],
-            "peak_note": "measured DFMA issue microbenchmark (osc_bench_fp64), lane-inst/s",
-        },
+        "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu,
+        "cpu_baseline_reference": cpu_py,
         "e2e": e2e,
         # + C5: rowscale, pack, unpack; C1/C2: the division classifier and the
         # two kernels of the launch-order partition (cub::DevicePartition)
@@ -848,6 +993,8 @@ def main():
     if world > 1 and backend != "nccl":
         line["note"] = f"{world} ranks over {backend} on {torch.cuda.device_count()} GPU(s): " \
                        "a multi-rank path check, not a scaling measurement"
+    if sharded_c3:
+        line["sharded_c3"] = sharded_c3
     if engine_line:
         line["equation_engine"] = engine_line
     if fma_line:

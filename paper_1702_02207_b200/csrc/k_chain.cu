@@ -28,12 +28,14 @@
 #include "osc_kernels.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 namespace osc {
 namespace {
 
 constexpr int kMaxWarps = 32;
+constexpr int kMaxDevices = 64;
 
 template <int K>
 struct Tile {
@@ -642,18 +644,40 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
 template <int K, int NT>
 constexpr size_t persist_smem() { return 2 * 4 * size_t(K) * NT * sizeof(double); }
 
-template <int K, int NT>
-cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
+// Resident CTAs of a persistent kernel on device `dev` (SMs x CTAs per SM),
+// computed once per kernel and device: the attribute call and the occupancy
+// query cost more host time than a short sharded period's launch itself.
+template <int K, int NT, bool kFma>
+int64_t persistent_ctas(int dev)
 {
-    int dev = 0, sms = 148, per_sm = 0;
-    cudaGetDevice(&dev);
+    static std::atomic<int64_t> cache[kMaxDevices];  // one per kernel instantiation
+    if (dev >= 0 && dev < kMaxDevices) {
+        const int64_t c = cache[dev].load(std::memory_order_relaxed);
+        if (c > 0)
+            return c;
+    }
+    auto kern = chain_tiles_persistent<K, NT, kFma>;
+    int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    auto kern = g.fma ? chain_tiles_persistent<K, NT, true> : chain_tiles_persistent<K, NT, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(persist_smem<K, NT>()));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, persist_smem<K, NT>());
+    const int64_t c = int64_t(sms) * std::max(per_sm, 1);
+    if (dev >= 0 && dev < kMaxDevices)
+        cache[dev].store(c, std::memory_order_relaxed);
+    return c;
+}
+
+template <int K, int NT>
+cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = g.fma ? chain_tiles_persistent<K, NT, true> : chain_tiles_persistent<K, NT, false>;
+    const int64_t ctas = g.fma ? persistent_ctas<K, NT, true>(dev)
+                               : persistent_ctas<K, NT, false>(dev);
     const int64_t ntiles = g.tiles * g.nbuf;
-    const int64_t grid = std::min<int64_t>(ntiles, int64_t(sms) * std::max(per_sm, 1));
+    const int64_t grid = std::min<int64_t>(ntiles, ctas);
     kern<<<static_cast<unsigned>(grid), NT, persist_smem<K, NT>(), stream>>>(g);
     return cudaGetLastError();
 }

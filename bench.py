@@ -277,7 +277,7 @@ class Workload:
             self.desc = workload_desc(name, world, transport, T)
             self.shard = None
             if world > 1 and transport == "nccl":
-                self.launches = 3 * self.launches  # interior + 2 edge launches per period
+                self.launches = 2 * self.launches  # interior + one edge launch per period
         elif name == "C5":
             # m, K built ONCE (rank 0: the QR of a 4096^2 draw) and broadcast;
             # rank r integrates trajectory columns [rN/G, (r+1)N/G)

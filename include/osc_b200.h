@@ -62,6 +62,15 @@ extern "C" {
  * when the call is captured into a CUDA graph (the check synchronises the
  * stream) and for per-period calls of a sharded run. */
 #define OSC_TRUSTED 2u
+/* flags (osc_rk4_chain_advance only): launch a subset of the shard's tiles.
+ * OSC_TILES_EDGES = the tiles that read a ghost zone or store into a
+ * neighbour (next to each ghost zone), OSC_TILES_INTERIOR = all the others;
+ * the two launches together equal one plain launch byte for byte (same tile
+ * geometry).  The NCCL transport runs the interior while the ghost exchange
+ * is in flight, then one launch covering both edges on the exchange's
+ * stream, concurrent with the interior's tail. */
+#define OSC_TILES_INTERIOR 4u
+#define OSC_TILES_EDGES 8u
 
 int osc_abi_version(void);
 const char *osc_last_error(void);

@@ -19,6 +19,8 @@ OSC_OK, OSC_NONFINITE, OSC_INVALID, OSC_CUDA_ERROR = 0, 1, 2, 3
 ABI_VERSION = 11
 OSC_FMA = 1
 OSC_TRUSTED = 2
+OSC_TILES_INTERIOR = 4
+OSC_TILES_EDGES = 8
 
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p

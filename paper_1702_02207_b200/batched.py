@@ -317,14 +317,17 @@ def chain_plan(B, s, nsteps, halo_steps=0) -> dict:
 
 
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None, fma=False, left=None, right=None, trusted=False, sync=None):
+                  stream=None, fma=False, left=None, right=None, trusted=False, sync=None,
+                  tiles=None):
     """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance).
 
     ``left``/``right``: optional ``(x, v, offset, count)`` -- a neighbour's
     next-input buffers (data pointers) that receive our boundary cells from
     the same kernel (the fused halo exchange).  ``sync``: optional
     ``(ready_left, ready_right, counters, period, timeout_ns)`` -- order the
-    edge tiles with the neighbours on the device (osc_edge_sync_t)."""
+    edge tiles with the neighbours on the device (osc_edge_sync_t).
+    ``tiles``: None (all), "interior" or "edges" -- the two subsets whose
+    launches together equal one (OSC_TILES_INTERIOR / OSC_TILES_EDGES)."""
     peers = []
     for p in (left, right):
         peers.append(ctypes.byref(_native.Peer(*p)) if p is not None else None)
@@ -336,7 +339,8 @@ def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
         _ptr(m), _ptr(C), _ptr(xin), _ptr(vin), _ptr(xout), _ptr(vout), m.numel(), int(own_lo),
         int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad), peers[0], peers[1],
         ctypes.byref(es) if es is not None else None,
-        (_native.OSC_FMA if fma else 0) | (_native.OSC_TRUSTED if trusted else 0),
+        (_native.OSC_FMA if fma else 0) | (_native.OSC_TRUSTED if trusted else 0)
+        | {None: 0, "interior": _native.OSC_TILES_INTERIOR, "edges": _native.OSC_TILES_EDGES}[tiles],
         ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_rk4_chain_advance", (m, C))
 

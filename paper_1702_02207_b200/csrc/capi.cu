@@ -252,8 +252,11 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
                           const osc_peer_t *left, const osc_peer_t *right,
                           const osc_edge_sync_t *sync, uint32_t flags, void *stream)
 {
-    if (flags & ~kRunFlags)
+    if (flags & ~kAdvanceFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
+    const uint32_t subset = flags & (OSC_TILES_INTERIOR | OSC_TILES_EDGES);
+    if (subset == (OSC_TILES_INTERIOR | OSC_TILES_EDGES))
+        return fail(OSC_INVALID, "OSC_TILES_INTERIOR and OSC_TILES_EDGES are exclusive");
     if (int rc = check_run_args(dt, nsteps, 1))
         return rc;
     if (n < 1 || own_lo < 0 || own_hi > n || own_lo >= own_hi)
@@ -300,12 +303,28 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
     if (sync) {
         if (!sync->counters || sync->timeout_ns < 0)
             return fail(OSC_INVALID, "bad edge sync descriptor");
+        if (subset)
+            return fail(OSC_INVALID, "edge sync orders whole launches: no tile subset");
         g.sync.ready[0] = sync->ready[0];
         g.sync.ready[1] = sync->ready[1];
         g.sync.ctr = sync->counters;
         g.sync.period = sync->period;
         g.sync.timeout_ns = sync->timeout_ns;
-        edge_sets(g, kTileK * kTileThreads, g.sync.nedge);
+    }
+    if (sync || subset) {
+        g.ordered = true;
+        edge_sets(g, kTileK * kTileThreads, g.nedge);
+        const int64_t rs = std::max(g.nedge[0], g.tiles - g.nedge[1]);
+        const int64_t nint = rs - g.nedge[0];  // interior tiles, walked first
+        if (subset == OSC_TILES_INTERIOR) {
+            g.walk0 = 0;
+            g.nwalk = nint;
+        } else if (subset == OSC_TILES_EDGES) {
+            g.walk0 = nint;
+            g.nwalk = g.tiles - nint;
+        }
+        if (subset && g.nwalk == 0)
+            return OSC_OK;  // an empty subset: nothing to launch
     }
     cudaError_t e = osc::launch_chain(g, kTileK, kTileThreads, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "chain_rk4_kernel");

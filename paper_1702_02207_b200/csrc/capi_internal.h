@@ -65,8 +65,10 @@ inline int check_run_args(double dt, int64_t nsteps, int64_t stride)
     return OSC_OK;
 }
 
-// Flags every integrate entry point accepts.
+// Flags every integrate entry point accepts (osc_rk4_chain_advance also
+// takes the tile subsets).
 constexpr uint32_t kRunFlags = OSC_FMA | OSC_TRUSTED;
+constexpr uint32_t kAdvanceFlags = kRunFlags | OSC_TILES_INTERIOR | OSC_TILES_EDGES;
 
 // How a flat parameter index maps to (system, cell) for the error message:
 // CellMajor = [s][B] (the batched 2-DOF SoA [2][B]: coordinate i / B of
@@ -298,8 +300,8 @@ inline void edge_sets(const osc::SegArgs &g, int64_t TILE, int64_t nedge[2])
     };
     nedge[0] = nedge[1] = 0;
     for (int side = 0; side < 2; ++side) {
-        if (!g.sync.ready[side] && !g.peer[side].x)
-            continue;  // no neighbour on this side
+        if (side == 0 ? g.own_lo == 0 : g.own_hi == g.n)
+            continue;  // no ghost zone on this side: a true chain end
         auto tile_at = [&](int64_t i) { return side == 0 ? i : g.tiles - 1 - i; };
         // the run of involved tiles from this side's end (own_start grows with
         // the tile, so the involvement of ordinary tiles ends with the run) ...

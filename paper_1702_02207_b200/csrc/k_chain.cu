@@ -147,9 +147,9 @@ __device__ __forceinline__ uint64_t globaltimer_ns()
 // interior tiles first, then the left-edge set, then the right-edge set.
 __device__ __forceinline__ int64_t tile_order(const SegArgs &g, int64_t it)
 {
-    if (!g.sync.ctr)
+    if (!g.ordered)
         return it;
-    const int64_t a = g.sync.nedge[0], b = g.sync.nedge[1];
+    const int64_t a = g.nedge[0], b = g.nedge[1];
     const int64_t rs = max(a, g.tiles - b);  // first tile of the right set
     const int64_t nint = rs - a;              // interior tiles (>= 0)
     if (it < nint)
@@ -163,7 +163,7 @@ __device__ __forceinline__ int edge_sides(const SegArgs &g, int64_t tile)
 {
     if (!g.sync.ctr)
         return 0;
-    return (tile < g.sync.nedge[0] ? 1 : 0) | (tile >= g.tiles - g.sync.nedge[1] ? 2 : 0);
+    return (tile < g.nedge[0] ? 1 : 0) | (tile >= g.tiles - g.nedge[1] ? 2 : 0);
 }
 
 // Thread 0, before an edge tile touches its inputs: wait until each involved
@@ -206,17 +206,18 @@ __device__ void edge_wait(const EdgeSync &s, int sides)
 // Thread 0, after every thread of an edge tile has stored (and fenced) its
 // cells: count the tile; the last edge tile of a side resets the tally for
 // the next launch and posts period + 1.
-__device__ void edge_done(const EdgeSync &s, int sides)
+__device__ void edge_done(const SegArgs &g, int sides)
 {
+    const EdgeSync &s = g.sync;
     for (int side = 0; side < 2; ++side) {
-        if (!((sides >> side) & 1) || s.nedge[side] == 0)
+        if (!((sides >> side) & 1) || g.nedge[side] == 0)
             continue;
         unsigned long long old;
         asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
                      : "=l"(old)
                      : "l"(&s.ctr[2 + side])
                      : "memory");
-        if (static_cast<int64_t>(old) + 1 == s.nedge[side]) {
+        if (static_cast<int64_t>(old) + 1 == g.nedge[side]) {
             s.ctr[2 + side] = 0;  // the next launch is stream-ordered after this one
             __threadfence_system();
             st_release_sys(&s.ctr[side], s.period + 1);
@@ -335,8 +336,9 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     constexpr bool kQ = K * kMaxT == 1024 && K >= 4;
     __shared__ Edges edges;
     __shared__ int s_skip;
-    const int64_t buf_id = blockIdx.x / g.tiles;
-    const int64_t tile = tile_order(g, blockIdx.x % g.tiles);
+    const int64_t nw = walk_tiles(g);
+    const int64_t buf_id = blockIdx.x / nw;
+    const int64_t tile = tile_order(g, g.walk0 + blockIdx.x % nw);
     const int sides = edge_sides(g, tile);
     // One read, broadcast: another CTA may record a divergence at any time,
     // and the exit must be uniform across this CTA's barriers.
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     __syncthreads();
     if (s_skip) {
         if (threadIdx.x == 0 && sides)
-            edge_done(g.sync, sides);  // nothing stored, but the neighbours must not stall
+            edge_done(g, sides);  // nothing stored, but the neighbours must not stall
         return;  // already diverged: state is unspecified, as integrate raised
     }
 
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
         __threadfence_system();  // our peer stores, before the post
         __syncthreads();
         if (threadIdx.x == 0)
-            edge_done(g.sync, sides);
+            edge_done(g, sides);
     }
 }
 
@@ -490,8 +492,9 @@ struct TileGeom {
 __device__ __forceinline__ TileGeom tile_geom(const SegArgs &g, int64_t it, int64_t TILE)
 {
     TileGeom tg;
-    tg.buf_id = it / g.tiles;
-    const int64_t tile = tile_order(g, it % g.tiles);
+    const int64_t nw = walk_tiles(g);
+    tg.buf_id = it / nw;
+    const int64_t tile = tile_order(g, g.walk0 + it % nw);
     tg.sides = edge_sides(g, tile);
     tg.own_start = g.own_lo + tile * g.W;
     tg.own_end = min(tg.own_start + g.W, g.own_hi);
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ int s_skip;
 
-    const int64_t ntiles = g.tiles * g.nbuf;
+    const int64_t ntiles = walk_tiles(g) * g.nbuf;
     edges_init(edges);
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
@@ -615,7 +618,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
         __syncthreads();  // every thread is done with buffer b; the results are in it
         if (threadIdx.x == 0) {
             if (tg.sides)  // post before waiting for the next tile (no wait cycle)
-                edge_done(g.sync, tg.sides);
+                edge_done(g, tg.sides);
             if (!s_skip) {
                 const int64_t o = tg.own_start - tg.L;
                 const unsigned bytes = static_cast<unsigned>(tg.own_end - tg.own_start) * 8u;
@@ -676,7 +679,7 @@ cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
     auto kern = g.fma ? chain_tiles_persistent<K, NT, true> : chain_tiles_persistent<K, NT, false>;
     const int64_t ctas = g.fma ? persistent_ctas<K, NT, true>(dev)
                                : persistent_ctas<K, NT, false>(dev);
-    const int64_t ntiles = g.tiles * g.nbuf;
+    const int64_t ntiles = walk_tiles(g) * g.nbuf;
     const int64_t grid = std::min<int64_t>(ntiles, ctas);
     kern<<<static_cast<unsigned>(grid), NT, persist_smem<K, NT>(), stream>>>(g);
     return cudaGetLastError();
@@ -687,7 +690,7 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
 {
     if (threads > max_threads<K>() || threads % 32)
         return cudaErrorInvalidConfiguration;
-    const int64_t blocks = g.tiles * g.nbuf;
+    const int64_t blocks = walk_tiles(g) * g.nbuf;
     const int64_t TILE = int64_t(threads) * K;
     const unsigned nb = static_cast<unsigned>(blocks);
     // Padding is needed only when a tile is longer than the whole buffer.

@@ -17,18 +17,15 @@ struct PeerGhost {
 };
 
 // In-kernel ordering of a shard's edge tiles with its neighbouring shards
-// (the multi-process fused exchange; include/osc_b200.h osc_edge_sync_t).
-// Tiles [0, nedge[0]) read the left ghost zone or store into the left
-// neighbour, tiles [tiles - nedge[1], tiles) likewise on the right; they run
-// LAST (interior tiles first), wait (bounded) until the neighbour's edge
-// counter reaches `period` before touching anything, and the last of them on
-// a side posts period + 1 into our counter for that side.
+// (the multi-process fused exchange; include/osc_b200.h osc_edge_sync_t):
+// the edge tiles (SegArgs::nedge) run LAST, wait (bounded) until the
+// neighbour's edge counter reaches `period` before touching anything, and
+// the last of them on a side posts period + 1 into our counter for that side.
 struct EdgeSync {
     const uint64_t *ready[2];  // neighbours' edge counters facing us (peer memory)
     uint64_t *ctr;             // ours: [0],[1] edge done; [2],[3] tallies; [4..7] timeout record
     uint64_t period;
     int64_t timeout_ns;
-    int64_t nedge[2];
 };
 
 // One launch of the chain kernel over nbuf buffers of n cells each.
@@ -47,7 +44,22 @@ struct SegArgs {
     bool fma;                // OSC_FMA mode (not bit-identical)
     PeerGhost peer[2];       // left / right neighbour ghost targets (x == nullptr: none)
     EdgeSync sync;           // sync.ctr == nullptr: no in-kernel ordering (stream/event order)
+    // Tile walk of a sharded buffer (nbuf == 1).  ordered: positions are
+    // mapped interior tiles first, then the left edge set [0, nedge[0]),
+    // then the right edge set [tiles - nedge[1], tiles) -- the tiles that
+    // read a ghost zone or store into a neighbour.  The launch covers walk
+    // positions [walk0, walk0 + nwalk) (nwalk == 0: all tiles), which is how
+    // the interior and the edges run as two launches on two streams.
+    bool ordered;
+    int64_t nedge[2];
+    int64_t walk0, nwalk;
 };
+
+// Tiles one buffer's launch walks.
+__host__ __device__ inline int64_t walk_tiles(const SegArgs &g)
+{
+    return g.nwalk ? g.nwalk : g.tiles;
+}
 
 // Fused compare (modal.py:141-162) at every retained sample of K1: ts are
 // the samples' time labels, sol the [8][B] analytic solutions, out the

@@ -101,13 +101,13 @@ def layout(s: int, rank: int, world: int, halo_steps: int) -> ShardLayout:
 
 
 def _cuda_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None, left=None, right=None, sync=None):
+                  stream=None, left=None, right=None, sync=None, tiles=None):
     from . import batched
 
     # the shard's parameters were validated once at construction
     batched.chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
                           first_bad, stream=stream, left=left, right=right, trusted=True,
-                          sync=sync)
+                          sync=sync, tiles=tiles)
 
 
 class ShardedChain:
@@ -117,9 +117,6 @@ class ShardedChain:
     copies its buffered slice.  ``advance`` defaults to the CUDA kernel; tests
     inject the oracle to check the exchange logic on CPU ranks.
     """
-
-    # interior/edge split: an edge region is at least one tile of owned cells
-    EDGE_CELLS = 4096  # >= any tile (K x threads) so interior tiles never slide into ghosts
 
     def __init__(self, m, C, x0, v0, dt, *, halo_steps=32, group=None, device=None,
                  advance=None, rank=None, world=None, transport="nccl", timeout_ms=None):
@@ -440,37 +437,29 @@ class ShardedChain:
         self.fill_ghosts(x, v, self.recv_l if left is not None else None,
                          self.recv_r if right is not None else None)
 
-    def _advance(self, xin, vin, xout, vout, lo, hi, n, step0, stream=None):
-        if hi > lo:
-            kw = {"stream": stream} if self.cuda else {}
-            self.advance(self.m, self.C, xin, vin, xout, vout, lo, hi, self.dt, n, step0,
-                         self.first_bad, **kw)
-
-    # -- one period of T steps, in three phases ------------------------------
-    def _split(self):
+    def _advance(self, n, step0, tiles=None, stream=None):
+        """One launch over the owned range; ``tiles`` = "interior" / "edges"
+        selects a subset of the same tile geometry (OSC_TILES_*), so the two
+        subset launches of a period equal one whole launch byte for byte."""
         a, b = self.L.own
-        return self.nranks > 1 and (b - a) > 2 * self.EDGE_CELLS + 2 * self.L.g
+        kw = {"stream": stream} if self.cuda else {}
+        if tiles is not None:
+            kw["tiles"] = tiles
+        self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, step0,
+                     self.first_bad, **kw)
 
+    # -- one period of T steps -------------------------------------------------
     def phase_interior(self, n, k):
-        """Launch the tiles that read no ghost cell (all of them if unsplit)."""
-        a, b = self.L.own
-        E = self.EDGE_CELLS
-        if self.nranks == 1:
-            self._advance(self.x, self.v, self.x2, self.v2, a, b, n, k)
-        elif self._split():
-            self._advance(self.x, self.v, self.x2, self.v2, a + E, b - E, n, k)
+        """Launch the tiles that read no ghost cell (all of them on one rank)."""
+        self._advance(n, k, tiles=None if self.world == 1 else "interior")
 
-    def phase_edges(self, n, k):
-        """After the ghost exchange: the tiles next to the ghost zones."""
-        a, b = self.L.own
-        E = self.EDGE_CELLS
-        if self.nranks == 1:
-            pass
-        elif self._split():
-            self._advance(self.x, self.v, self.x2, self.v2, a, a + E, n, k)
-            self._advance(self.x, self.v, self.x2, self.v2, b - E, b, n, k)
-        else:
-            self._advance(self.x, self.v, self.x2, self.v2, a, b, n, k)
+    def phase_edges(self, n, k, stream=None):
+        """After the ghost exchange: ONE launch covering the tiles next to both
+        ghost zones (the same tile geometry as the interior launch)."""
+        if self.world > 1:
+            self._advance(n, k, tiles="edges", stream=stream)
+
+    def _swap(self):
         self.x, self.x2 = self.x2, self.x
         self.v, self.v2 = self.v2, self.v
 
@@ -480,32 +469,41 @@ class ShardedChain:
 
     def run(self, nsteps: int):
         """Advance the shard nsteps steps; returns the 1-based first bad step
-        of the WHOLE chain (min over ranks) or 0."""
+        of the WHOLE chain (min over ranks) or 0.
+
+        NCCL transport, per period: the interior launch goes on the main
+        stream; the ghost exchange (NCCL P2P of 2 x g doubles per neighbour)
+        and then one launch covering both edges go on a side stream that
+        waited for the previous period only, so exchange and edge tiles run
+        concurrently with the interior and its tail; the main stream waits
+        for the edges before the next period."""
         if self.transport == "peer" and self.world > 1 and self.peer_bufs:
             self._run_peer(nsteps)
             return self._reduce_first_bad()
         k = 0
+        t_host = time.perf_counter()
+        periods = 0
         while k < nsteps:
             n = min(self.T, nsteps - k)
             if self.world > 1 and self.cuda:
-                # The exchange needs only the previous period's output, not the
-                # interior tiles: it waits on an event recorded BEFORE they are
-                # enqueued, so it overlaps them (interior tiles read owned cells
-                # only; the exchange reads boundary cells and writes ghosts).
                 main = torch.cuda.current_stream(self.device)
                 ready = torch.cuda.Event()
-                ready.record(main)
+                ready.record(main)  # the previous period's output is complete
                 self.phase_interior(n, k)
                 self.comm_stream.wait_event(ready)
                 with torch.cuda.stream(self.comm_stream):
                     self._exchange(self.x, self.v)
+                    self.phase_edges(n, k, stream=self.comm_stream)
                 main.wait_stream(self.comm_stream)
             else:
                 self.phase_interior(n, k)
                 if self.world > 1:
                     self._exchange(self.x, self.v)
-            self.phase_edges(n, k)
+                    self.phase_edges(n, k)
+            self._swap()
             k += n
+            periods += 1
+        self.host_s_per_period = (time.perf_counter() - t_host) / max(periods, 1)
         return self._reduce_first_bad()
 
     def _reduce_first_bad(self) -> int:
@@ -594,6 +592,7 @@ class LocalShardGroup:
                 p.fill_ghosts(p.x, p.v, left, right)
             for p in self.parts:
                 p.phase_edges(n, k)
+                p._swap()
             k += n
         bad = [int(p.first_bad.item()) for p in self.parts]
         bad = [b for b in bad if b > 0]

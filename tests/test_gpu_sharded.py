@@ -163,3 +163,32 @@ def test_peer_transport_across_runs_with_odd_periods():
     ref = batched.integrate_chains(m, C, x0, v0, 1e-3, 3 * T + 5 * T + 3 + T + 2 * T)
     assert bits(x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
     assert bits(v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())
+
+
+@pytest.mark.parametrize("n,own,T", [(300_000, (64, 299_936), 32),
+                                     (40_001, (40, 39_961), 20),
+                                     (5_000, (12, 4_988), 6),
+                                     (2_100, (0, 2_050), 25),
+                                     (1_800, (30, 1_800), 8)])
+def test_tile_subsets_equal_one_launch(n, own, T):
+    """OSC_TILES_INTERIOR + OSC_TILES_EDGES (the NCCL transport's two
+    launches, same tile geometry) == one whole launch, byte for byte, and the
+    interior launch reads no ghost cell (poisoned ghosts leave it exact)."""
+    m, C, x0, v0 = (torch.from_numpy(a).cuda() for a in _chain(n, n))
+    a, b = own
+    fb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    whole_x, whole_v = torch.zeros_like(x0), torch.zeros_like(v0)
+    batched.chain_advance(m, C, x0, v0, whole_x, whole_v, a, b, 1e-3, T, 0, fb)
+    # interior with NaN ghosts: must not read them
+    xg, vg = x0.clone(), v0.clone()
+    xg[:a] = float("nan")
+    vg[:a] = float("nan")
+    xg[b:] = float("nan")
+    vg[b:] = float("nan")
+    sub_x, sub_v = torch.zeros_like(x0), torch.zeros_like(v0)
+    batched.chain_advance(m, C, xg, vg, sub_x, sub_v, a, b, 1e-3, T, 0, fb, tiles="interior")
+    batched.chain_advance(m, C, x0, v0, sub_x, sub_v, a, b, 1e-3, T, 0, fb, tiles="edges")
+    torch.cuda.synchronize()
+    assert int(fb.item()) == 0
+    assert bits(sub_x[a:b].cpu().numpy()) == bits(whole_x[a:b].cpu().numpy())
+    assert bits(sub_v[a:b].cpu().numpy()) == bits(whole_v[a:b].cpu().numpy())

@@ -22,10 +22,13 @@ pytestmark = pytest.mark.timeout(300)
 
 
 def oracle_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                   **_):
+                   tiles=None, **_):
     """Same contract as osc_rk4_chain_advance, on the CPU oracle: the buffer is
     treated as its own chain (wall at cell 0, free at n-1); only the owned
-    cells are written and checked."""
+    cells are written and checked.  ``tiles``: "interior" writes only the
+    owned cells farther than 2*nsteps cells from a ghost zone (they cannot
+    depend on a ghost), "edges" the rest -- the contract of the OSC_TILES_*
+    subsets (together one launch; the interior reads no ghost)."""
     x, v = xin.numpy().copy(), vin.numpy().copy()
     m, C = m.numpy(), C.numpy()
     for j in range(nsteps):
@@ -37,8 +40,16 @@ def oracle_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0
             if fb == 0 or fb > step0 + j + 1:
                 first_bad.fill_(step0 + j + 1)
             break
-    xout[own_lo:own_hi] = torch.from_numpy(x[own_lo:own_hi])
-    vout[own_lo:own_hi] = torch.from_numpy(v[own_lo:own_hi])
+    n = xin.numel()
+    keep = np.zeros(n, dtype=bool)
+    keep[own_lo:own_hi] = True
+    if tiles is not None:
+        r = 2 * nsteps
+        inner = np.zeros(n, dtype=bool)
+        inner[own_lo + (r if own_lo > 0 else 0):own_hi - (r if own_hi < n else 0)] = True
+        keep &= inner if tiles == "interior" else ~inner
+    xout[keep] = torch.from_numpy(x[keep])
+    vout[keep] = torch.from_numpy(v[keep])
 
 
 def _chain(s, seed, stiff=None):
@@ -58,7 +69,7 @@ def _free_port():
         return sock.getsockname()[1]
 
 
-def _worker(rank, world, port, s, nsteps, T, edge, stiff, q):
+def _worker(rank, world, port, s, nsteps, T, stiff, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -66,7 +77,6 @@ def _worker(rank, world, port, s, nsteps, T, edge, stiff, q):
         m, C, x0, v0 = _chain(s, 11, stiff)
         sh = sharded.ShardedChain(m, C, x0, v0, 1e-3, halo_steps=T, device=torch.device("cpu"),
                                   advance=oracle_advance)
-        sh.EDGE_CELLS = edge
         fb = sh.run(nsteps)
         x, v = sh.gather()
         if rank == 0:
@@ -75,8 +85,8 @@ def _worker(rank, world, port, s, nsteps, T, edge, stiff, q):
         dist.destroy_process_group()
 
 
-def _run_world(world, s, nsteps, T, edge=64, stiff=None):
-    return collect(_worker, (world, _free_port(), s, nsteps, T, edge, stiff), world)
+def _run_world(world, s, nsteps, T, stiff=None):
+    return collect(_worker, (world, _free_port(), s, nsteps, T, stiff), world)
 
 
 def test_layout():
@@ -116,8 +126,6 @@ def test_local_group_matches_single_chain():
     m, C, x0, v0 = _chain(s, 5)
     grp = sharded.LocalShardGroup(m, C, x0, v0, 1e-3, 4, halo_steps=6,
                                   device=torch.device("cpu"), advance=oracle_advance)
-    for p in grp.parts:
-        p.EDGE_CELLS = 100  # exercise the interior/edge split on small shards
     assert grp.run(45) == 0
     x, v = grp.gather()
     _, _, xo, vo, _ = oracle.c_rk4_chains(m[None], C[None], x0[None], v0[None], 1e-3, 45,

@@ -36,6 +36,11 @@ namespace {
 
 constexpr int kMaxWarps = 32;
 constexpr int kMaxDevices = 64;
+#ifndef OSC_PERSIST_BUFS
+#define OSC_PERSIST_BUFS 3
+#endif
+constexpr int kPersistBufs = OSC_PERSIST_BUFS;  // tile buffers of the persistent kernel (see there)
+static_assert(kPersistBufs == 2 || kPersistBufs == 3, "2 or 3 tile buffers");
 
 template <int K>
 struct Tile {
@@ -526,16 +531,22 @@ template <int K, int NT, bool kFma>
 __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_persistent(SegArgs g)
 {
     constexpr int64_t TILE = int64_t(NT) * K;
-    extern __shared__ __align__(128) double tbuf[];  // 2 x [m | C | x | v] x TILE
+    // kPersistBufs x [m | C | x | v] x TILE.  Three buffers: tile i computes
+    // in buffer i % 3 while tile i + 1's inputs sit loaded in the next one and
+    // tile i - 1's results still drain from the third by bulk store, so the
+    // refill at the end of tile i (tile i + 2, into the buffer tile i - 1
+    // used) waits for a store issued a whole tile earlier, not for the one it
+    // just issued.
+    extern __shared__ __align__(128) double tbuf[];
     __shared__ Edges edges;
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t bars[kPersistBufs];
     __shared__ int s_skip;
 
     const int64_t ntiles = walk_tiles(g) * g.nbuf;
     edges_init(edges);
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int b = 0; b < kPersistBufs; ++b)
+            mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int b = 0; b < 2; ++b) {
             const int64_t it = blockIdx.x + int64_t(b) * gridDim.x;
@@ -554,11 +565,10 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
     t.lastj = -1;
     t.validn = K;
     const int cl = threadIdx.x * K;  // first cell of this thread within the tile
-    int i = 0;
+    int i = 0, b = 0, use = 0;  // b = i % kPersistBufs, use = i / kPersistBufs
     for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x, ++i) {
-        const int b = i & 1;
         double *sm = tbuf + b * 4 * TILE;
-        mbar_wait(&bars[b], (i >> 1) & 1);
+        mbar_wait(&bars[b], use & 1);
         const TileGeom tg = tile_geom(g, it, TILE);
         const int64_t c0 = tg.L + cl;
         if (threadIdx.x == 0)  // uniform skip decision (see chain_rk4_kernel)
@@ -616,10 +626,11 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();  // every thread is done with buffer b; the results are in it
+        const bool stored = !s_skip;
         if (threadIdx.x == 0) {
             if (tg.sides)  // post before waiting for the next tile (no wait cycle)
                 edge_done(g, tg.sides);
-            if (!s_skip) {
+            if (stored) {
                 const int64_t o = tg.own_start - tg.L;
                 const unsigned bytes = static_cast<unsigned>(tg.own_end - tg.own_start) * 8u;
                 const int64_t go = tg.base + tg.own_start;
@@ -630,14 +641,24 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                     bulk_s2g(g.vs + go, sm + 3 * TILE + o, bytes);
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                // the buffer is refilled below: its reads must be done
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
             const int64_t nx = it + 2 * int64_t(gridDim.x);
             if (nx < ntiles) {
+                // tile i + 2 goes into the buffer tile i - 1 used: its store
+                // group must have finished reading it (the group just
+                // committed for tile i may stay in flight)
+                if (stored && kPersistBufs == 3)
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                else
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                const int nb = kPersistBufs == 2 ? b : (b == 0 ? kPersistBufs - 1 : b - 1);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_tile<K, NT>(g, nx, sm, &bars[b]);
+                issue_tile<K, NT>(g, nx, tbuf + nb * 4 * TILE, &bars[nb]);
             }
+        }
+        if (++b == kPersistBufs) {
+            b = 0;
+            ++use;
         }
     }
     if (threadIdx.x == 0)
@@ -645,7 +666,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
 }
 
 template <int K, int NT>
-constexpr size_t persist_smem() { return 2 * 4 * size_t(K) * NT * sizeof(double); }
+constexpr size_t persist_smem() { return kPersistBufs * 4 * size_t(K) * NT * sizeof(double); }
 
 // Resident CTAs of a persistent kernel on device `dev` (SMs x CTAs per SM),
 // computed once per kernel and device: the attribute call and the occupancy

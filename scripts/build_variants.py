@@ -16,6 +16,7 @@ VARIANTS = {
     "u1": ["-DOSC_B2_UNROLL=1"],
     "u2": ["-DOSC_B2_UNROLL=2"],
     "u8": ["-DOSC_B2_UNROLL=8"],
+    "pb2": ["-DOSC_PERSIST_BUFS=2"],  # K3 double-buffered (round 1) vs 3 buffers
 }
 
 if __name__ == "__main__":

@@ -277,18 +277,19 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
     }
 }
 
-// Store an owned cell: own output, optional sample slot, and -- for cells in
-// a neighbour's ghost range -- straight into that neighbour's next-input
-// buffer (the fused compute + halo exchange over peer memory).
-__device__ __forceinline__ void store_owned(const SegArgs &g, int64_t base, int64_t c, double x,
-                                            double v)
+// Does owned range [lo, hi) store anything into a neighbour's ghost zone?
+// Uniform per tile: the per-cell range tests below run only where it does
+// (the edge tiles of a sharded run), not in every tile of every launch.
+__device__ __forceinline__ bool touches_peer(const SegArgs &g, int64_t lo, int64_t hi)
 {
-    g.xout[base + c] = x;
-    g.vout[base + c] = v;
-    if (g.xs) {
-        g.xs[base + c] = x;
-        g.vs[base + c] = v;
-    }
+    return (g.peer[0].x && lo < g.peer[0].hi && hi > g.peer[0].lo) ||
+           (g.peer[1].x && lo < g.peer[1].hi && hi > g.peer[1].lo);
+}
+
+// Neighbour ghost copies of an owned cell c (the fused exchange of the peer
+// transport): straight into the neighbour's next-input buffer.
+__device__ __forceinline__ void store_peers(const SegArgs &g, int64_t c, double x, double v)
+{
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
         const PeerGhost &p = g.peer[side];
@@ -415,8 +416,22 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int64_t c = c0 + j;
-        if (c >= own_start && c < own_end)
-            store_owned(g, base, c, x[j], v[j]);
+        if (c >= own_start && c < own_end) {
+            g.xout[base + c] = x[j];
+            g.vout[base + c] = v[j];
+            if (g.xs) {
+                g.xs[base + c] = x[j];
+                g.vs[base + c] = v[j];
+            }
+        }
+    }
+    if (touches_peer(g, own_start, own_end)) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int64_t c = c0 + j;
+            if (c >= own_start && c < own_end)
+                store_peers(g, c, x[j], v[j]);
+        }
     }
     if (sides) {
         __threadfence_system();  // our peer stores, before the post
@@ -475,20 +490,6 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
-// Neighbour ghost copies of an owned cell (the fused exchange of the peer
-// transport); the owned output itself leaves with the tile's bulk copy.
-__device__ __forceinline__ void store_peers(const SegArgs &g, int64_t c, double x, double v)
-{
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-        const PeerGhost &p = g.peer[side];
-        if (p.x && c >= p.lo && c < p.hi) {
-            p.x[c + p.offset] = x;
-            p.v[c + p.offset] = v;
-        }
-    }
-}
-
 struct TileGeom {
     int64_t buf_id, base, L, own_start, own_end;
     int sides;  // edge-sync sides of the tile (edge_sides)
@@ -497,9 +498,11 @@ struct TileGeom {
 __device__ __forceinline__ TileGeom tile_geom(const SegArgs &g, int64_t it, int64_t TILE)
 {
     TileGeom tg;
+    // one buffer (every tiled run but batches of long chains): no 64-bit
+    // division in the tile transition
     const int64_t nw = walk_tiles(g);
-    tg.buf_id = it / nw;
-    const int64_t tile = tile_order(g, g.walk0 + it % nw);
+    tg.buf_id = g.nbuf == 1 ? 0 : it / nw;
+    const int64_t tile = tile_order(g, g.walk0 + (g.nbuf == 1 ? it : it % nw));
     tg.sides = edge_sides(g, tile);
     tg.own_start = g.own_lo + tile * g.W;
     tg.own_end = min(tg.own_start + g.W, g.own_hi);
@@ -615,11 +618,16 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             // of 16 strided 8-byte stores per thread.
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                const int64_t c = c0 + j;
                 sm[2 * TILE + cl + j] = x[j];
                 sm[3 * TILE + cl + j] = v[j];
-                if (c >= tg.own_start && c < tg.own_end)
-                    store_peers(g, c, x[j], v[j]);
+            }
+            if (touches_peer(g, tg.own_start, tg.own_end)) {
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int64_t c = c0 + j;
+                    if (c >= tg.own_start && c < tg.own_end)
+                        store_peers(g, c, x[j], v[j]);
+                }
             }
             if (tg.sides)
                 __threadfence_system();  // our peer stores, before the post

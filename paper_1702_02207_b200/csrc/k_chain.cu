@@ -490,6 +490,72 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
+// A thread's K contiguous cells of one tile array in shared memory, moved as
+// 16-byte chunks in a lane-rotated order: at instruction j lane L touches
+// chunk (j + rot) % (K/2), rot = (L >> 1) % (K/2).  Plain ascending order puts
+// 16 lanes of a warp on one 16-byte bank group (the cells of a thread are 64
+// bytes apart lane to lane): 4x the wavefronts of a conflict-free access
+// (ncu: "L1 Wavefronts Shared Excessive" 3/4 of every tile load and store).
+// The rotation is undone with selects, two stages for K = 8.
+template <int K>
+__device__ __forceinline__ int chunk_rot()
+{
+    return static_cast<int>((threadIdx.x >> 1) & (K / 2 - 1));
+}
+
+template <int K>
+__device__ __forceinline__ void lds_cells(const double *p, double (&out)[K])
+{
+    static_assert(K == 8 || K == 4, "rotated tile access for K = 4 or 8");
+    constexpr int NC = K / 2;
+    const int rot = chunk_rot<K>();
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    double2 c[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+        c[j] = q[(j + rot) & (NC - 1)];  // c[j] = chunk (j + rot)
+#pragma unroll
+    for (int b = 1; b < NC; b <<= 1) {  // chunk k = c[(k - rot) % NC]
+        double2 t[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+            t[k] = (rot & b) ? c[(k - b) & (NC - 1)] : c[k];
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+            c[k] = t[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        out[2 * k] = c[k].x;
+        out[2 * k + 1] = c[k].y;
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void sts_cells(double *p, const double (&in)[K])
+{
+    constexpr int NC = K / 2;
+    const int rot = chunk_rot<K>();
+    double2 c[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+        c[k] = make_double2(in[2 * k], in[2 * k + 1]);
+#pragma unroll
+    for (int b = 1; b < NC; b <<= 1) {  // c[j] = chunk (j + rot)
+        double2 t[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+            t[k] = (rot & b) ? c[(k + b) & (NC - 1)] : c[k];
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+            c[k] = t[k];
+    }
+    double2 *q = reinterpret_cast<double2 *>(p);
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+        q[(j + rot) & (NC - 1)] = c[j];
+}
+
 struct TileGeom {
     int64_t buf_id, base, L, own_start, own_end;
     int sides;  // edge-sync sides of the tile (edge_sides)
@@ -579,19 +645,18 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
         __syncthreads();
         if (!s_skip) {
             bool ok = true;
+            double mj[K];
+            lds_cells<K>(sm + cl, mj);
+            lds_cells<K>(sm + TILE + cl, t.C);
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                t.C[j] = sm[TILE + cl + j];
-                t.md[j] = make_divisor(sm[cl + j]);
+                t.md[j] = make_divisor(mj[j]);
                 ok &= kFma ? divisor_fast_ok(t.md[j]) : divisor_range_ok(t.md[j]);
             }
             t.Cn = (cl + K < TILE) ? sm[TILE + cl + K] : 1.0;
             double x[K], v[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                x[j] = sm[2 * TILE + cl + j];
-                v[j] = sm[3 * TILE + cl + j];
-            }
+            lds_cells<K>(sm + 2 * TILE + cl, x);
+            lds_cells<K>(sm + 3 * TILE + cl, v);
             // single-test division here (div_fastq): -5% instructions, C3
             // +1.1%; the whole-chain kernel keeps div_fast, whose schedule
             // ptxas handles better (profiles/r01/README.md)
@@ -599,11 +664,8 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 step<K, false, kFma ? Arith::Fma : Arith::FastQ>(t, x, v, g.k, edges, ok);
             if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                 // exact replay from the tile input still in shared memory
-#pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    x[j] = sm[2 * TILE + cl + j];
-                    v[j] = sm[3 * TILE + cl + j];
-                }
+                lds_cells<K>(sm + 2 * TILE + cl, x);
+                lds_cells<K>(sm + 3 * TILE + cl, v);
                 for (int64_t s = 0; s < g.nsteps; ++s) {
                     step<K, false, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, edges, ok);
                     if (__syncthreads_or(owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
@@ -616,11 +678,8 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             // The tile input is no longer needed: the results go into its x/v
             // slots and leave as one bulk copy per array (TMA store) instead
             // of 16 strided 8-byte stores per thread.
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                sm[2 * TILE + cl + j] = x[j];
-                sm[3 * TILE + cl + j] = v[j];
-            }
+            sts_cells<K>(sm + 2 * TILE + cl, x);
+            sts_cells<K>(sm + 3 * TILE + cl, v);
             if (touches_peer(g, tg.own_start, tg.own_end)) {
 #pragma unroll
                 for (int j = 0; j < K; ++j) {

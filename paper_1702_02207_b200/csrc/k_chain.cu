@@ -622,8 +622,14 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             if (it < ntiles)
                 issue_tile<K, NT>(g, it, tbuf + b * 4 * TILE, &bars[b]);
         }
+        // one buffer: the skip decision is launch-invariant (diverged_before
+        // reads the state at launch start), so it is read once, not per tile
+        // behind a barrier every warp waits at
+        if (g.nbuf == 1)
+            s_skip = diverged_before(g, 0);
     }
     __syncthreads();
+    const bool skip_once = g.nbuf == 1 && s_skip != 0;
 
     Tile<K> t;
     t.lane = threadIdx.x & 31;
@@ -640,10 +646,14 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
         mbar_wait(&bars[b], use & 1);
         const TileGeom tg = tile_geom(g, it, TILE);
         const int64_t c0 = tg.L + cl;
-        if (threadIdx.x == 0)  // uniform skip decision (see chain_rk4_kernel)
-            s_skip = diverged_before(g, tg.buf_id);
-        __syncthreads();
-        if (!s_skip) {
+        bool skip = skip_once;
+        if (g.nbuf > 1) {
+            if (threadIdx.x == 0)  // uniform skip decision (see chain_rk4_kernel)
+                s_skip = diverged_before(g, tg.buf_id);
+            __syncthreads();
+            skip = s_skip != 0;
+        }
+        if (!skip) {
             bool ok = true;
             double mj[K];
             lds_cells<K>(sm + cl, mj);
@@ -693,7 +703,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();  // every thread is done with buffer b; the results are in it
-        const bool stored = !s_skip;
+        const bool stored = !skip;
         if (threadIdx.x == 0) {
             if (tg.sides)  // post before waiting for the next tile (no wait cycle)
                 edge_done(g, tg.sides);

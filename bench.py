@@ -843,7 +843,11 @@ def main():
 
     sharded_c3 = None
     if world > 1 and args.config == "C2" and not args.no_sharded_c3:
-        sharded_c3 = sharded_c3_record(rank, world, device, backend, local)
+        # a side record: a failure here is reported, not fatal to the line
+        try:
+            sharded_c3 = sharded_c3_record(rank, world, device, backend, local)
+        except Exception as exc:  # noqa: BLE001
+            sharded_c3 = {"error": f"{type(exc).__name__}: {exc}"[:500]}
 
     fma_line = None
     if wl.name in ("C2", "C3", "C4") and world == 1:

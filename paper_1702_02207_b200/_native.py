@@ -136,12 +136,18 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     return lib
 
 
-def lib() -> ctypes.CDLL:
-    """The library, after checking a CUDA device is present."""
-    import torch
+_DEVICE_OK = False
 
-    if not torch.cuda.is_available():
-        raise NativeUnavailableError("no CUDA device: the B200 path has no CPU fallback")
+
+def lib() -> ctypes.CDLL:
+    """The library, after checking (once) that a CUDA device is present."""
+    global _DEVICE_OK
+    if not _DEVICE_OK:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeUnavailableError("no CUDA device: the B200 path has no CPU fallback")
+        _DEVICE_OK = True
     return load()
 
 

@@ -22,6 +22,8 @@ struct HostCtx {
     cudaStream_t st[3] = {nullptr, nullptr, nullptr};
     unsigned char *pin = nullptr;
     size_t pin_cap = 0;
+    unsigned char *dmem = nullptr;  // the staged calls' device block, grown as needed
+    size_t dmem_cap = 0;
 
     ~HostCtx()
     {
@@ -36,6 +38,8 @@ struct HostCtx {
                 cudaStreamDestroy(s);
         if (pin)
             cudaFreeHost(pin);
+        if (dmem)
+            cudaFree(dmem);
         cudaSetDevice(prev);
         cudaGetLastError();
     }
@@ -60,6 +64,23 @@ int host_ctx(HostCtx *&out)
     return OSC_OK;
 }
 
+int device_block(HostCtx &c, size_t bytes, unsigned char *&p)
+{
+    if (c.dmem_cap < bytes) {
+        if (c.dmem) {
+            OSC_CUDA(cudaStreamSynchronize(c.st[0]));  // the block's last user is done
+            OSC_CUDA(cudaFree(c.dmem));
+        }
+        c.dmem = nullptr;
+        c.dmem_cap = 0;
+        const size_t cap = std::max<size_t>(bytes, size_t(1) << 16);
+        OSC_CUDA(cudaMalloc(reinterpret_cast<void **>(&c.dmem), cap));
+        c.dmem_cap = cap;
+    }
+    p = c.dmem;
+    return OSC_OK;
+}
+
 int staging(HostCtx &c, size_t bytes, unsigned char *&p)
 {
     if (c.pin_cap < bytes) {
@@ -76,54 +97,56 @@ int staging(HostCtx &c, size_t bytes, unsigned char *&p)
 }
 
 // A small host-pointer call, as one round trip through the pinned staging
-// buffer: the inputs go up in one copy, the parameter rule is checked ON
-// THE DEVICE in the same stream as the work (no extra synchronisation), the
-// outputs and the check result come back in one copy, and only then is
-// anything written to the caller's buffers -- an invalid system returns
-// OSC_INVALID with the caller's outputs untouched.
+// buffer: the inputs go up in one copy (with the check record's two slots
+// pre-set to ~0, so no memset), the parameter rule is checked ON THE DEVICE
+// in the same stream as the work -- fused into the work's own kernel where
+// it supports it (`fused`), else one param_check launch -- the outputs and
+// the check record come back in one copy, and only then is anything written
+// to the caller's buffers: an invalid system returns OSC_INVALID with the
+// caller's outputs untouched.  Device block and stream are cached per thread.
 //
 // Layout (device block and staging alike, all 8-byte slots):
-//   [ inputs (in_slots) | outputs (out_slots) | badp[2] ]
-// `work` enqueues the computation given the device block; `check` names the
-// parameter arrays to validate (slot offsets into the block, n elements).
+//   [ inputs (in_slots) | badp[2] | outputs (out_slots) ]
+// `work(d, st, badp)` enqueues the computation given the device block; when
+// `fused` it applies the parameter rule to m = d + m_off, C = d + C_off itself.
 template <class Work>
 int staged_call(size_t in_slots, size_t out_slots, size_t m_off, size_t C_off, int64_t nparam,
                 const std::vector<std::pair<const void *, size_t>> &ins,
                 const std::vector<std::pair<void *, size_t>> &outs, Work work,
-                const double *hm, const double *hC, ParamLayout layout, int64_t B, int64_t s)
+                const double *hm, const double *hC, ParamLayout layout, int64_t B, int64_t s,
+                bool fused = false)
 {
     HostCtx *c = nullptr;
     if (int rc = host_ctx(c))
         return rc;
     cudaStream_t st = c->st[0];
-    const size_t slots = in_slots + out_slots + 2;
-    unsigned char *pin = nullptr;
+    const size_t slots = in_slots + 2 + out_slots;
+    unsigned char *pin = nullptr, *dmem = nullptr;
     if (int rc = staging(*c, slots * 8, pin))
         return rc;
-    unsigned char *dmem = nullptr;
-    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&dmem), slots * 8, st));
-    Scratch guard;  // frees dmem (stream-ordered) on every return path
-    guard.p = reinterpret_cast<double *>(dmem);
-    guard.s = st;
+    if (int rc = device_block(*c, slots * 8, dmem))
+        return rc;
     size_t off = 0;
     for (auto &[p, n] : ins) {
         std::memcpy(pin + off, p, n);
         off += n;
     }
-    OSC_CUDA(cudaMemcpyAsync(dmem, pin, in_slots * 8, cudaMemcpyHostToDevice, st));
+    std::memset(pin + in_slots * 8, 0xff, 16);  // the check record: "no offender"
+    OSC_CUDA(cudaMemcpyAsync(dmem, pin, (in_slots + 2) * 8, cudaMemcpyHostToDevice, st));
     double *d = reinterpret_cast<double *>(dmem);
-    auto *badp = reinterpret_cast<unsigned long long *>(d + in_slots + out_slots);
-    OSC_CUDA(osc::launch_param_check(d + m_off, d + C_off, nparam, badp, st));
-    if (int rc = work(d, st))
+    auto *badp = reinterpret_cast<unsigned long long *>(d + in_slots);
+    if (!fused && nparam > 0)
+        OSC_CUDA(osc::launch_param_check(d + m_off, d + C_off, nparam, badp, st, false));
+    if (int rc = work(d, st, badp))
         return rc;
     OSC_CUDA(cudaMemcpyAsync(pin + in_slots * 8, d + in_slots, (out_slots + 2) * 8,
                              cudaMemcpyDeviceToHost, st));
     OSC_CUDA(cudaStreamSynchronize(st));
     unsigned long long bad[2];
-    std::memcpy(bad, pin + (in_slots + out_slots) * 8, sizeof bad);
+    std::memcpy(bad, pin + in_slots * 8, sizeof bad);
     if (bad[0] != ~0ull || bad[1] != ~0ull)  // the first offender in the caller's layout
         return host_param_fail(hm, hC, nparam, layout, B, s);
-    off = in_slots * 8;
+    off = (in_slots + 2) * 8;
     for (auto &[p, n] : outs) {
         if (p)
             std::memcpy(p, pin + off, n);
@@ -162,9 +185,9 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     if ((4 * cells + out_slots) * 8 <= kStagedMax) {
         unsigned long long worst[2] = {~0ull, ~0ull};
         const size_t sb = nsamp * bytes;
-        auto work = [&](double *d, cudaStream_t st) -> int {
+        auto work = [&](double *d, cudaStream_t st, unsigned long long *) -> int {
             double *dm = d, *dC = d + cells, *dx = d + 2 * cells, *dv = d + 3 * cells;
-            double *o = d + 4 * cells;  // the output slots
+            double *o = d + 4 * cells + 2;  // the output slots (after the check record)
             OSC_CUDA(cudaMemcpyAsync(o, dx, 2 * bytes, cudaMemcpyDeviceToDevice, st));
             double *ox = o, *ov = o + cells;
             int64_t *fb = reinterpret_cast<int64_t *>(o + 2 * cells);
@@ -359,14 +382,14 @@ int osc_derivative_host(const double *m, const double *C, const double *x, doubl
     if (!m || !C || !x || !dvel)
         return fail(OSC_INVALID, "null buffer");
     const size_t cells = static_cast<size_t>(B * s), bytes = cells * sizeof(double);
-    auto work = [&](double *d, cudaStream_t st) -> int {
-        OSC_CUDA(osc::launch_derivative(d, d + cells, d + 2 * cells, d + 3 * cells, B, s,
-                                        cell_major != 0, st));
+    auto work = [&](double *d, cudaStream_t st, unsigned long long *bad) -> int {
+        OSC_CUDA(osc::launch_derivative(d, d + cells, d + 2 * cells, d + 3 * cells + 2, B, s,
+                                        cell_major != 0, st, bad));
         return OSC_OK;
     };
     return staged_call(3 * cells, cells, 0, cells, static_cast<int64_t>(cells),
                        {{m, bytes}, {C, bytes}, {x, bytes}}, {{dvel, bytes}}, work, m, C,
-                       cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s);
+                       cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s, true);
 }
 
 int osc_energy_host(const double *m, const double *C, const double *x, const double *v,
@@ -379,15 +402,15 @@ int osc_energy_host(const double *m, const double *C, const double *x, const dou
     if (!m || !C || !x || !v || !out)
         return fail(OSC_INVALID, "null buffer");
     const size_t cells = static_cast<size_t>(B * s), bytes = cells * sizeof(double);
-    auto work = [&](double *d, cudaStream_t st) -> int {
-        OSC_CUDA(osc::launch_energy(d, d + cells, d + 2 * cells, d + 3 * cells, d + 4 * cells, B,
-                                    s, cell_major != 0, st));
+    auto work = [&](double *d, cudaStream_t st, unsigned long long *bad) -> int {
+        OSC_CUDA(osc::launch_energy(d, d + cells, d + 2 * cells, d + 3 * cells,
+                                    d + 4 * cells + 2, B, s, cell_major != 0, st, bad));
         return OSC_OK;
     };
     return staged_call(4 * cells, static_cast<size_t>(B), 0, cells, static_cast<int64_t>(cells),
                        {{m, bytes}, {C, bytes}, {x, bytes}, {v, bytes}},
                        {{out, B * sizeof(double)}}, work, m, C,
-                       cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s);
+                       cell_major ? ParamLayout::CellMajor : ParamLayout::Chains, B, s, true);
 }
 
 }  // extern "C"

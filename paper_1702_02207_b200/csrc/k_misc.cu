@@ -13,16 +13,31 @@ namespace {
 
 // Cells of chain b are at x[b*chain_stride + i*cell_stride]: [B][s] uses
 // (s, 1); the batched 2-DOF SoA layout [2][B] uses (1, B).
+// bad (may be null): the parameter rule fused in (param_check_kernel's
+// out[2] contract, flat indices into m / C) -- every cell is one thread's.
+__device__ __forceinline__ void check_cell(const double *m, const double *C, int64_t c,
+                                           unsigned long long *bad)
+{
+    if (!bad)
+        return;
+    const double a = m[c], b = C[c];
+    if (!(a > 0.0 && a <= DBL_MAX))
+        atomicMin(&bad[0], static_cast<unsigned long long>(c));
+    if (!(b > 0.0 && b <= DBL_MAX))
+        atomicMin(&bad[1], static_cast<unsigned long long>(c));
+}
+
 __global__ void derivative_kernel(const double *__restrict__ m, const double *__restrict__ C,
                                   const double *__restrict__ x, double *__restrict__ dvel,
                                   int64_t B, int64_t s, int64_t chain_stride,
-                                  int64_t cell_stride)
+                                  int64_t cell_stride, unsigned long long *bad)
 {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid >= B * s)
         return;
     const int64_t b = gid / s, i = gid % s;
     const int64_t o = b * chain_stride;
+    check_cell(m, C, o + i * cell_stride, bad);
     const auto at = [&](const double *p, int64_t j) { return p[o + j * cell_stride]; };
     // acceleration_at, oscillator.py:160-164, literally.
     const double left = sub(at(x, i), i > 0 ? at(x, i - 1) : 0.0);
@@ -35,7 +50,8 @@ __global__ void derivative_kernel(const double *__restrict__ m, const double *__
 __global__ void energy_kernel(const double *__restrict__ m, const double *__restrict__ C,
                               const double *__restrict__ x, const double *__restrict__ v,
                               double *__restrict__ out, int64_t B, int64_t s,
-                              int64_t chain_stride, int64_t cell_stride)
+                              int64_t chain_stride, int64_t cell_stride,
+                              unsigned long long *bad)
 {
     const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (b >= B)
@@ -45,6 +61,7 @@ __global__ void energy_kernel(const double *__restrict__ m, const double *__rest
     double prev = 0.0;
     for (int64_t i = 0; i < s; ++i) {
         const int64_t c = o + i * cell_stride;
+        check_cell(m, C, c, bad);
         const double vi = v[c], xi = x[c];
         total = add(total, mul(mul(mul(0.5, m[c]), vi), vi));
         const double ext = sub(xi, prev);  // pos[i] - (pos[i-1] if i > 0 else 0.0)
@@ -315,16 +332,18 @@ __global__ void param_check_kernel(const double *__restrict__ m, const double *_
 }
 
 cudaError_t launch_param_check(const double *m, const double *C, int64_t n,
-                               unsigned long long *out, cudaStream_t stream)
+                               unsigned long long *out, cudaStream_t stream, bool init)
 {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 8, (n + 255) / 256)));
-    cudaError_t e = cudaMemsetAsync(out, 0xff, 2 * sizeof(unsigned long long), stream);
-    if (e != cudaSuccess)
-        return e;
+    if (init) {
+        cudaError_t e = cudaMemsetAsync(out, 0xff, 2 * sizeof(unsigned long long), stream);
+        if (e != cudaSuccess)
+            return e;
+    }
     if (n > 0)
         param_check_kernel<<<grid, 256, 0, stream>>>(m, C, n, out);
     return cudaGetLastError();
@@ -371,26 +390,27 @@ cudaError_t launch_fp64_peak(int64_t iters, int mode, double *sink, int64_t *lan
 }
 
 cudaError_t launch_derivative(const double *m, const double *C, const double *x, double *dvel,
-                              int64_t B, int64_t s, bool cell_major, cudaStream_t stream)
+                              int64_t B, int64_t s, bool cell_major, cudaStream_t stream,
+                              unsigned long long *bad)
 {
     const int64_t total = B * s;
     if (total == 0)
         return cudaSuccess;
     const int threads = 256;
     derivative_kernel<<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0,
-                        stream>>>(m, C, x, dvel, B, s, cell_major ? 1 : s, cell_major ? B : 1);
+                        stream>>>(m, C, x, dvel, B, s, cell_major ? 1 : s, cell_major ? B : 1, bad);
     return cudaGetLastError();
 }
 
 cudaError_t launch_energy(const double *m, const double *C, const double *x, const double *v,
                           double *out, int64_t B, int64_t s, bool cell_major,
-                          cudaStream_t stream)
+                          cudaStream_t stream, unsigned long long *bad)
 {
     if (B == 0)
         return cudaSuccess;
     const int threads = 128;
     energy_kernel<<<static_cast<unsigned>((B + threads - 1) / threads), threads, 0, stream>>>(
-        m, C, x, v, out, B, s, cell_major ? 1 : s, cell_major ? B : 1);
+        m, C, x, v, out, B, s, cell_major ? 1 : s, cell_major ? B : 1, bad);
     return cudaGetLastError();
 }
 

@@ -83,13 +83,16 @@ cudaError_t launch_compare_batch2(const double *sol, const double *xs, const dou
 
 cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stream);
 
-// cell_major: [s][B] layout (the batched 2-DOF SoA); else [B][s].
+// cell_major: [s][B] layout (the batched 2-DOF SoA); else [B][s].  bad (may
+// be null, else pre-set to ~0): the parameter rule fused into the same launch
+// (launch_param_check's out[2] contract).
 cudaError_t launch_derivative(const double *m, const double *C, const double *x, double *dvel,
-                              int64_t B, int64_t s, bool cell_major, cudaStream_t stream);
+                              int64_t B, int64_t s, bool cell_major, cudaStream_t stream,
+                              unsigned long long *bad = nullptr);
 
 cudaError_t launch_energy(const double *m, const double *C, const double *x, const double *v,
                           double *out, int64_t B, int64_t s, bool cell_major,
-                          cudaStream_t stream);
+                          cudaStream_t stream, unsigned long long *bad = nullptr);
 
 // Earliest divergence of a batch on the device: out[0] = min positive step,
 // out[1] = its smallest index (both ~0 when nothing diverged).
@@ -98,8 +101,9 @@ cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *o
 
 // Parameter rule of OscillatorSystem (oscillator.py:75-80): out[0] / out[1]
 // = smallest index of an invalid mass / spring rate (~0 when none).
+// init = false: out[] is already ~0 (staged host calls upload it).
 cudaError_t launch_param_check(const double *m, const double *C, int64_t n,
-                               unsigned long long *out, cudaStream_t stream);
+                               unsigned long long *out, cudaStream_t stream, bool init = true);
 
 cudaError_t launch_div2_classify(const double *b, int64_t n, uint8_t *pass, cudaStream_t stream);
 

@@ -380,13 +380,19 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
     // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
     // overrides it for benchmarking (read-only process state).
     int ns = kBatch2NS, threads = kBatch2Threads;
-    // Too few systems to fill the GPU: one system per thread keeps each
-    // thread's serial recurrence short (C1 is a single latency-bound system).
+    // Fewer systems than ~2048 per SM (the per-rank slices of C2 at 4 and 8
+    // GPUs: 2^18, 2^17): one system per thread in 128-thread CTAs -- many
+    // small CTAs, no partly filled last wave.  Measured on B200
+    // (scripts/k1_split_sweep.py, profiles/r02/k1_split.txt): 2^18 systems
+    // 3.64e11 -> 4.07e11 DOF-steps/s, 2^17 3.49e11 -> 3.95e11; 2^19 and 2^20
+    // keep NS=2 x 256.  C1 (a single latency-bound system) stays below.
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (B < int64_t(sms) * 1024)
+    if (B < int64_t(sms) * 2048) {
         ns = 1;
+        threads = 128;
+    }
     if (B <= int64_t(sms) * 32)
         threads = 32;  // at most one warp per SM anyway: the latency build
     if (const char *e = std::getenv("OSC_B2")) {

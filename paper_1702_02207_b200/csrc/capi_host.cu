@@ -186,7 +186,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         unsigned long long worst[2] = {~0ull, ~0ull};
         const size_t sb = nsamp * bytes;
         auto work = [&](double *d, cudaStream_t st, unsigned long long *) -> int {
-            double *dm = d, *dC = d + cells, *dx = d + 2 * cells, *dv = d + 3 * cells;
+            double *dm = d, *dC = d + cells, *dx = d + 2 * cells;  // x, v adjacent
             double *o = d + 4 * cells + 2;  // the output slots (after the check record)
             OSC_CUDA(cudaMemcpyAsync(o, dx, 2 * bytes, cudaMemcpyDeviceToDevice, st));
             double *ox = o, *ov = o + cells;

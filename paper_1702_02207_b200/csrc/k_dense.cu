@@ -63,6 +63,15 @@ __device__ __forceinline__ int swz128(int row, int k)
     return row * BK + ((((k >> 1) ^ (row & 7))) << 1) + (k & 1);
 }
 
+// Fragment row order within an 8-row group: lane group a (= lane / 4) of an
+// m8n8k4 fragment takes tile row perm8(a) = 2(a % 4) + a / 4.  A 64-bit
+// shared load is served per half-warp (a = 0..3 or 4..7): with the rows
+// {0,2,4,6} (resp. {1,3,5,7}) the swizzle XOR (row % 8) moves the two 16-byte
+// chunks a fragment row reads to 8 distinct chunks -- conflict-free -- where
+// rows {0,1,2,3} would pair them up (2-way conflicts, ncu: 2x wavefronts).
+// The accumulator rows / columns follow the same order (epilogue staging).
+__device__ __forceinline__ int perm8(int a) { return ((a & 3) << 1) | (a >> 2); }
+
 __device__ __forceinline__ unsigned smem_addr(const void *p)
 {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -160,11 +169,13 @@ __global__ void __launch_bounds__(THREADS, 4)
     __syncthreads();
 
     const int ar = lane >> 2, ac = lane & 3;  // fragment coordinates
-    // Fragment offsets within a stage: A rows wm*32 + 8i + ar at k = 4q + ac;
-    // B columns wn*16 + 8j + ar (rows of the [cols][k] box) at k = 4q + ac.
-    const auto offa = [&](int q, int i) { return swz128(wm * 32 + i * 8 + ar, 4 * q + ac); };
+    const int pr = perm8(ar);
+    // Fragment offsets within a stage: A rows wm*32 + 8i + perm8(ar) at
+    // k = 4q + ac; B columns wn*16 + 8j + perm8(ar) (rows of the [cols][k]
+    // box) at k = 4q + ac.
+    const auto offa = [&](int q, int i) { return swz128(wm * 32 + i * 8 + pr, 4 * q + ac); };
     const auto offb = [&](int q, int j) {
-        return BM * BK + swz128(wn * 16 + j * 8 + ar, 4 * q + ac);
+        return BM * BK + swz128(wn * 16 + j * 8 + pr, 4 * q + ac);
     };
     for (int kt = 0; kt < KT; ++kt) {
         mbar_wait(&full[kt % STAGES], (kt / STAGES) & 1);
@@ -207,14 +218,16 @@ __global__ void __launch_bounds__(THREADS, 4)
     // thread sees both halves (stage j and j+1) of its trajectories.
     double *sC = smem;
     constexpr int CS = BN + 1;
+    // accumulator (row ar, columns 2ac, 2ac + 1) of each 8 x 8 block is tile
+    // row perm8(ar), tile columns perm8(2ac), perm8(2ac + 1)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const int r = wm * 32 + i * 8 + ar;
-            const int c = wn * 16 + j * 8 + 2 * ac;
-            sC[r * CS + c] = acc[i][j][0];
-            sC[r * CS + c + 1] = acc[i][j][1];
+            const int r = wm * 32 + i * 8 + pr;
+            const int c = wn * 16 + j * 8;
+            sC[r * CS + c + perm8(2 * ac)] = acc[i][j][0];
+            sC[r * CS + c + perm8(2 * ac + 1)] = acc[i][j][1];
         }
     __syncthreads();
 

@@ -398,7 +398,7 @@ int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, d
     cudaStreamDestroy(side);  // released once its queued work is done
     if (e != cudaSuccess)
         return cuda_fail(e, "dense_rk4_gemm");
-    e = osc::launch_dense_unpack(BA, Vp, X, V, s, N, sp, stream);
+    e = osc::launch_dense_unpack(BA, Vp, X, V, s, N, Np, stream);
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "unpack_kernel");
 }
 

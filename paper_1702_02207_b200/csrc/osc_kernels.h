@@ -125,9 +125,8 @@ cudaError_t launch_dense_steps(const double *A, double *BA, double *BB, double *
                                double *SV, int64_t *first_bad, int64_t sp, int64_t Np,
                                StepConsts k, int64_t step0, int64_t nsteps, cudaStream_t stream,
                                cudaStream_t side = nullptr);
-// BA [2Np][sp] and Vp [Np][sp] are trajectory-major (k_dense.cu).
 cudaError_t launch_dense_unpack(const double *BA, const double *Vp, double *X, double *V,
-                                int64_t s, int64_t N, int64_t sp, cudaStream_t stream);
+                                int64_t s, int64_t N, int64_t Np, cudaStream_t stream);
 
 cudaError_t launch_equation_engine(const double *m, const double *C, const double *x0,
                                    const double *v0, int s, double dt, int64_t nsteps,

@@ -19,7 +19,7 @@ namespace {
 // all their outputs in ONE device-to-host copy.
 struct HostCtx {
     int dev = -1;
-    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t st[4] = {nullptr, nullptr, nullptr, nullptr};  // [3]: parameter uploads
     unsigned char *pin = nullptr;
     size_t pin_cap = 0;
     unsigned char *dmem = nullptr;  // the staged calls' device block, grown as needed
@@ -270,60 +270,78 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     const auto H2D = cudaMemcpyHostToDevice;
     const auto D2H = cudaMemcpyDeviceToHost;
 
-    // Parameters first: every chunk's m and C go up (in the chunk's device
-    // layout) and are checked in one device pass before any state is copied
-    // or integrated, so an invalid system returns OSC_INVALID with the
-    // caller's buffers untouched (the reference rejects it at construction,
-    // oscillator.py:66-80).  Costs the m/C upload's overlap with compute.
-    for (int64_t c = 0; c < nchunk; ++c) {
-        const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
-        if (chains) {
-            const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
-            OSC_CUDA(cudaMemcpyAsync(dm + o, m + o, n, H2D, streams[0]));
-            OSC_CUDA(cudaMemcpyAsync(dC + o, C + o, n, H2D, streams[0]));
-        } else {
-            const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
-            for (int r = 0; r < 2; ++r) {
-                OSC_CUDA(cudaMemcpyAsync(dm + o + r * nb, m + r * B + b0, n, H2D, streams[0]));
-                OSC_CUDA(cudaMemcpyAsync(dC + o + r * nb, C + r * B + b0, n, H2D, streams[0]));
-            }
+    // The parameter rule without giving up the overlap: chunk by chunk, m and
+    // C go up on the parameter stream, the chunk's state on its own stream
+    // (after its m, C: an event), then its kernels -- so the copy engine sees
+    // m0 C0 x0 v0 m1 ... and chunk 0 starts computing at once.  After the
+    // last m, C the parameter stream checks all of them in one device pass.
+    // The host waits for that check (it ends ~1 ms in, chunk 0 computes for
+    // ~50/nchunk ms) and only then enqueues the device-to-host copies: an
+    // invalid call returns OSC_INVALID with the caller's buffers untouched
+    // (the reference rejects it at construction, oscillator.py:66-80).
+    cudaStream_t pst = ctx->st[3];
+    struct Events {
+        std::vector<cudaEvent_t> ev;
+        ~Events()
+        {
+            for (auto e : ev)
+                cudaEventDestroy(e);
         }
-    }
-    {
-        int64_t bad[2];
-        if (int rc = scan_params(dm, dC, static_cast<int64_t>(cells), streams[0], bad))
-            return rc;
-        if (bad[0] >= 0 || bad[1] >= 0)  // the first offender in the caller's layout
-            return host_param_fail(m, C, static_cast<int64_t>(cells), layout, B, s);
-    }
-
+    } evs;
+    evs.ev.resize(nchunk + 1, nullptr);
+    for (auto &e : evs.ev)
+        OSC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    OSC_CUDA(cudaEventRecord(evs.ev[nchunk], streams[0]));  // scratch allocated
+    OSC_CUDA(cudaStreamWaitEvent(pst, evs.ev[nchunk], 0));
     for (int64_t c = 0; c < nchunk; ++c) {
         cudaStream_t st = streams[c % nstream];
         const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
-        int rc;
         if (chains) {
-            // [B][s]: a chunk of chains is one contiguous block per array
             const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
+            OSC_CUDA(cudaMemcpyAsync(dm + o, m + o, n, H2D, pst));
+            OSC_CUDA(cudaMemcpyAsync(dC + o, C + o, n, H2D, pst));
+            OSC_CUDA(cudaEventRecord(evs.ev[c], pst));
+            OSC_CUDA(cudaStreamWaitEvent(st, evs.ev[c], 0));
             OSC_CUDA(cudaMemcpyAsync(dx + o, x + o, n, H2D, st));
             OSC_CUDA(cudaMemcpyAsync(dv + o, v + o, n, H2D, st));
-            rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps, stride, dxs,
-                                dvs, nullptr, dfb + b0, 0, OSC_TRUSTED, st);
-            if (rc != OSC_OK)
+            if (int rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps,
+                                        stride, dxs, dvs, nullptr, dfb + b0, 0, OSC_TRUSTED, st))
                 return rc;
-            OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));
-            OSC_CUDA(cudaMemcpyAsync(v + o, dv + o, n, D2H, st));
         } else {
             // [2][B]: the chunk is packed as its own [2][nb] block on the device
             const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
+            for (int r = 0; r < 2; ++r) {
+                OSC_CUDA(cudaMemcpyAsync(dm + o + r * nb, m + r * B + b0, n, H2D, pst));
+                OSC_CUDA(cudaMemcpyAsync(dC + o + r * nb, C + r * B + b0, n, H2D, pst));
+            }
+            OSC_CUDA(cudaEventRecord(evs.ev[c], pst));
+            OSC_CUDA(cudaStreamWaitEvent(st, evs.ev[c], 0));
             const double *hs[2] = {x, v};
             double *ds[2] = {dx, dv};
             for (int a = 0; a < 2; ++a)
                 for (int r = 0; r < 2; ++r)
                     OSC_CUDA(cudaMemcpyAsync(ds[a] + o + r * nb, hs[a] + r * B + b0, n, H2D, st));
-            rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride, dxs, dvs,
-                                nullptr, dfb + b0, OSC_TRUSTED, st);
-            if (rc != OSC_OK)
+            if (int rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride,
+                                        dxs, dvs, nullptr, dfb + b0, OSC_TRUSTED, st))
                 return rc;
+        }
+    }
+    {
+        int64_t bad[2];
+        if (int rc = scan_params(dm, dC, static_cast<int64_t>(cells), pst, bad))
+            return rc;  // (synchronises the parameter stream only)
+        if (bad[0] >= 0 || bad[1] >= 0)  // the first offender in the caller's layout
+            return host_param_fail(m, C, static_cast<int64_t>(cells), layout, B, s);
+    }
+    for (int64_t c = 0; c < nchunk; ++c) {
+        cudaStream_t st = streams[c % nstream];
+        const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
+        if (chains) {
+            const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
+            OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));
+            OSC_CUDA(cudaMemcpyAsync(v + o, dv + o, n, D2H, st));
+        } else {
+            const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
             for (int r = 0; r < 2; ++r) {
                 OSC_CUDA(cudaMemcpyAsync(x + r * B + b0, dx + o + r * nb, n, D2H, st));
                 OSC_CUDA(cudaMemcpyAsync(v + r * B + b0, dv + o + r * nb, n, D2H, st));

@@ -244,6 +244,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         {
             for (int i = 0; i < n; ++i)
                 cudaStreamSynchronize(st[i]);  // every stream is done with mem
+            cudaStreamSynchronize(st[3]);      // the parameter / result-copy stream
             if (mem) {
                 cudaFreeAsync(mem, st[0]);
                 cudaStreamSynchronize(st[0]);
@@ -288,7 +289,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
                 cudaEventDestroy(e);
         }
     } evs;
-    evs.ev.resize(nchunk + 1, nullptr);
+    evs.ev.resize(2 * nchunk + 1, nullptr);  // [c]: m, C of chunk c up; [nchunk + 1 + c]: its kernels done
     for (auto &e : evs.ev)
         OSC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     OSC_CUDA(cudaEventRecord(evs.ev[nchunk], streams[0]));  // scratch allocated
@@ -307,6 +308,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
             if (int rc = osc_rk4_chains(dm + o, dC + o, dx + o, dv + o, nb, s, dt, nsteps,
                                         stride, dxs, dvs, nullptr, dfb + b0, 0, OSC_TRUSTED, st))
                 return rc;
+            OSC_CUDA(cudaEventRecord(evs.ev[nchunk + 1 + c], st));
         } else {
             // [2][B]: the chunk is packed as its own [2][nb] block on the device
             const size_t o = static_cast<size_t>(2 * b0), n = static_cast<size_t>(nb) * 8;
@@ -324,6 +326,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
             if (int rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride,
                                         dxs, dvs, nullptr, dfb + b0, OSC_TRUSTED, st))
                 return rc;
+            OSC_CUDA(cudaEventRecord(evs.ev[nchunk + 1 + c], st));
         }
     }
     {
@@ -333,8 +336,11 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         if (bad[0] >= 0 || bad[1] >= 0)  // the first offender in the caller's layout
             return host_param_fail(m, C, static_cast<int64_t>(cells), layout, B, s);
     }
+    // results leave on the (now idle) parameter stream, each chunk as soon as
+    // its kernels are done -- not behind the later chunks queued on its stream
     for (int64_t c = 0; c < nchunk; ++c) {
-        cudaStream_t st = streams[c % nstream];
+        cudaStream_t st = pst;
+        OSC_CUDA(cudaStreamWaitEvent(st, evs.ev[nchunk + 1 + c], 0));
         const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
         if (chains) {
             const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
@@ -366,6 +372,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     OSC_CUDA(cudaMemcpyAsync(worst, dworst, sizeof worst, D2H, streams[0]));
     for (int i = 0; i < nstream; ++i)
         OSC_CUDA(cudaStreamSynchronize(streams[i]));
+    OSC_CUDA(cudaStreamSynchronize(pst));  // the result copies
     if (worst[0] != ~0ull)
         return fail(OSC_NONFINITE, "integration diverged at step %lld (system %lld)",
                     (long long)worst[0], (long long)worst[1]);

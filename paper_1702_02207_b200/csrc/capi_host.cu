@@ -220,12 +220,14 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     // -- large: chunked multi-stream pipeline ---------------------------------
     // Chunking, so that only the first chunk's H2D and the last one's D2H are
     // exposed: >= 2 MB of state per chunk, at most 8 chunks; 2-DOF chunks
-    // keep >= 148*1024 systems so each launch keeps K1's throughput shape.
+    // keep >= 148*2048 systems so each launch keeps K1's two-systems-per-
+    // thread shape (smaller batches switch to one per thread, which is right
+    // for a lone small batch but 4% slower when chunks run side by side).
     int64_t nchunk = 1;
     if (!xs && B > 1)
         nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 21)}));
     if (!chains)
-        nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 1024)));
+        nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 2048)));
     if (const char *e = std::getenv("OSC_HOST_CHUNKS")) {  // benchmarking knob
         const long long n = std::atoll(e);
         if (!xs && n >= 1 && n <= 64)

@@ -56,8 +56,17 @@ int host_ctx(HostCtx *&out)
         ctx.resize(dev + 1);
     HostCtx &c = ctx[dev];
     if (c.dev < 0) {
-        for (auto &s : c.st)
-            OSC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        // Chunk streams in descending priority (chunk c runs on stream c % 3):
+        // the GPU finishes chunk 0 first, so its results copy back while later
+        // chunks compute, and the lower-priority chunks fill the earlier ones'
+        // tail waves.  The parameter / result-copy stream gets the highest.
+        int lo = 0, hi = 0;  // numerically: lo = least, hi = greatest priority
+        OSC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int step = (lo - hi) >= 2 ? 1 : 0;
+        const int p[4] = {hi + 0 * step, hi + 1 * step, hi + 2 * step, hi};
+        for (int i = 0; i < 4; ++i)
+            OSC_CUDA(cudaStreamCreateWithPriority(&c.st[i], cudaStreamNonBlocking,
+                                                  std::min(p[i], lo)));
         c.dev = dev;
     }
     out = &c;

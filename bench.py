@@ -262,7 +262,10 @@ class Workload:
             sl = workloads.part(workloads.C4_B, rank, world)
             arrays = tuple(np.ascontiguousarray(a[sl]) for a in arrays)
             self.kernel = "chain_rk4_kernel<8>"
-            self.launches = -(-p.nsteps // 512)
+            # whole-chain launches of 512 steps; batches of >= 1024 chains run
+            # as two halves on two streams (capi.cu): two launches per 512 steps
+            halves = 2 if arrays[0].shape[0] >= 1024 else 1
+            self.launches = halves * -(-p.nsteps // 512)
             self.desc = workload_desc(name, world)
         elif name == "C3":
             arrays = workloads.c3()
@@ -286,7 +289,11 @@ class Workload:
             sl = workloads.part(workloads.C5_N, rank, world)
             arrays = arrays[:2] + tuple(np.ascontiguousarray(a[:, sl]) for a in arrays[2:])
             self.kernel = "dense_rk4_gemm"
-            self.launches = 2 * p.nsteps  # + rowscale, pack, unpack (counted in gpu_launches)
+            # 2 GEMMs per step, each as two halves of column tiles on two streams
+            # when there are >= 16 column tiles of 32 (k_dense.cu); + rowscale,
+            # pack, unpack in gpu_launches
+            self.gemm_halves = 2 if 2 * (workloads.C5_N // world) // 32 >= 16 else 1
+            self.launches = 2 * self.gemm_halves * p.nsteps
             self.desc = workload_desc(name, world)
         elif name == "C1":
             arrays = workloads.c1()
@@ -761,9 +768,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--halo", type=int, default=0, help="C3 steps per tiled launch")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
-                    help="C3 multi-GPU ghost exchange: NCCL P2P, or peer-memory stores "
-                         "fused into the tile kernel")
+    ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
+                    help="C3 multi-GPU ghost exchange: peer-memory stores fused into the "
+                         "tile kernel (default), or NCCL P2P (the library baseline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sharded-c3", action="store_true",
@@ -913,8 +920,10 @@ def main():
     achieved = alg_bytes / launch_s / 1e9
     traffic = ncu_traffic(wl.kernel, wl.name)
     if wl.name == "C5":
-        # GEMM launches dominate: 2 per RK4 step, each [s x s] x [s x 2N]
-        gemm_flops = 2.0 * workloads.C5_S * workloads.C5_S * 2 * workloads.C5_N
+        # GEMM launches dominate: 2 per RK4 step, each [s x s] x [s x 2N] run
+        # as gemm_halves launches of column tiles
+        gemm_flops = (2.0 * workloads.C5_S * workloads.C5_S * 2 * (workloads.C5_N // world)
+                      / wl.gemm_halves)
         launch_s = dev_s / (args.steps * wl.launches)
         dmma = fp64_peak(local, mode=2)
         achieved_tf = gemm_flops / launch_s / 1e12

@@ -91,13 +91,10 @@ int osc_validate_parameters(const double *m, const double *C, int64_t n, int64_t
                             void *stream);
 int osc_last_invalid_parameter(int *which, int64_t *index);
 
-/* Process-wide side effect: entry points that need scratch memory
- * (osc_rk4_batch2 and its compare form -- the launch order of the
- * two-operation division --, osc_rk4_chains, osc_rk4_dense, the *_host
- * forms) allocate it
- * stream-ordered from the device's default memory pool and raise that pool's
- * release threshold once per device (cudaMemPoolAttrReleaseThreshold), so
- * repeated calls reuse the memory instead of re-mapping it. */
+/* Scratch memory: entry points that need it allocate it stream-ordered from a
+ * memory pool the library owns (one per device, created on first use, which
+ * keeps freed blocks for the next call).  The device's default pool -- the
+ * host application's cudaMallocAsync -- is not touched. */
 
 /* Batched independent 2-DOF systems (paper eq. 2), SoA layout [2][B]:
  * m, C, x, v hold coordinate 0 of all B systems, then coordinate 1.

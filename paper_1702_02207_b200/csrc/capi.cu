@@ -29,7 +29,6 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
         if (int rc = check_params(m, C, 2 * B, static_cast<cudaStream_t>(stream),
                                   ParamLayout::CellMajor, B))
             return rc;
-    retain_pool_memory();
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs, es,
                                        first_bad, (flags & OSC_FMA) != 0,
                                        static_cast<cudaStream_t>(stream));
@@ -56,7 +55,6 @@ int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *
                                   ParamLayout::CellMajor, B))
             return rc;
     const osc::CmpArgs cmp{ts, sol, report};
-    retain_pool_memory();
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, nullptr, nullptr,
                                        nullptr, first_bad, (flags & OSC_FMA) != 0,
                                        static_cast<cudaStream_t>(stream), &cmp);
@@ -147,10 +145,9 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
         if (e != cudaSuccess)
             return cuda_fail(e, "energy_kernel");
     }
-    retain_pool_memory();
     Scratch scratch;
     scratch.s = stream;
-    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch.p), 2 * bytes, stream));
+    OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&scratch.p), 2 * bytes, stream));
 
     // The time loop over chains [b0, b0 + nb) on stream st.
     auto run_group = [&](int64_t b0, int64_t nb, cudaStream_t st) -> int {
@@ -368,7 +365,6 @@ int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, d
         return OSC_OK;
     if (!A || !X || !V || !first_bad)
         return fail(OSC_INVALID, "null buffer");
-    retain_pool_memory();
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     const int64_t sp = osc::dense_pad_s(s), Np = osc::dense_pad_n(N);
     const size_t op = static_cast<size_t>(sp) * 2 * Np, st = static_cast<size_t>(sp) * Np;
@@ -376,7 +372,7 @@ int osc_rk4_dense(const double *A, double *X, double *V, int64_t s, int64_t N, d
     const size_t total = 2 * op + 3 * st + (pad_a ? static_cast<size_t>(sp) * sp : 0);
     Scratch ws;
     ws.s = stream;
-    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws.p), total * sizeof(double), stream));
+    OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&ws.p), total * sizeof(double), stream));
     double *BA = ws.p, *BB = BA + op, *Vp = BB + op, *SX = Vp + st, *SV = SX + st;
     const double *Ause = A;
     if (pad_a) {
@@ -491,7 +487,7 @@ int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches,
 {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     unsigned long long *d = nullptr;
-    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d), sizeof *d, stream));
+    OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&d), sizeof *d, stream));
     OSC_CUDA(cudaMemsetAsync(d, 0, sizeof *d, stream));
     cudaError_t e = osc::launch_check_division(n, seed, mode, d, stream);
     if (e != cudaSuccess)

@@ -182,7 +182,6 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         return OSC_OK;
     if (!m || !C || !x || !v || !first_bad || (!xs) != (!vs))
         return fail(OSC_INVALID, "null buffer");
-    retain_pool_memory();
     const size_t cells = static_cast<size_t>(B * s);
     const size_t bytes = cells * sizeof(double);
     const size_t nsamp = xs ? static_cast<size_t>(1 + nsteps / stride) : 0;
@@ -264,7 +263,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     } cleanup{streams, nstream};
 
     const size_t total = 4 * bytes + B * sizeof(int64_t) + 2 * nsamp * bytes + 16;
-    OSC_CUDA(cudaMallocAsync(&cleanup.mem, total, streams[0]));
+    OSC_CUDA(osc::scratch_alloc(&cleanup.mem, total, streams[0]));
     cudaEvent_t ready;
     OSC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     OSC_CUDA(cudaEventRecord(ready, streams[0]));

@@ -85,7 +85,7 @@ inline int scan_params(const double *m, const double *C, int64_t n, cudaStream_t
     if (n <= 0)
         return OSC_OK;
     unsigned long long *d = nullptr;
-    OSC_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d), 2 * sizeof *d, stream));
+    OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&d), 2 * sizeof *d, stream));
     unsigned long long h[2] = {~0ull, ~0ull};
     cudaError_t e = osc::launch_param_check(m, C, n, d, stream);
     if (e == cudaSuccess)
@@ -315,23 +315,6 @@ inline void edge_sets(const osc::SegArgs &g, int64_t TILE, int64_t nedge[2])
                 k = g.tiles;
         nedge[side] = k;
     }
-}
-
-// Keep freed stream-ordered allocations in the device's default pool instead
-// of returning them to the driver at every synchronisation (the default
-// release threshold is 0), so repeated host-API calls do not re-map memory.
-inline void retain_pool_memory()
-{
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev)
-        return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    done_dev = dev;
 }
 
 struct Scratch {

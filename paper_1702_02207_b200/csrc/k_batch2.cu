@@ -419,7 +419,7 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
             return e;
         const size_t off_cls = size_t(B + 1) * sizeof(int64_t);  // mcls [2][B], sys [B]
         const size_t off_tmp = (off_cls + 3 * size_t(B) + 255) & ~size_t(255);
-        if ((e = cudaMallocAsync(&scratch, off_tmp + temp, stream)) != cudaSuccess)
+        if ((e = scratch_alloc(&scratch, off_tmp + temp, stream)) != cudaSuccess)
             return e;
         char *p = static_cast<char *>(scratch);
         int64_t *order = reinterpret_cast<int64_t *>(p);

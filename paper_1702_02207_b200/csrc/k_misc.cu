@@ -6,6 +6,7 @@
 #include "osc_kernels.h"
 
 #include <algorithm>
+#include <mutex>
 #include <cfloat>
 
 namespace osc {
@@ -329,6 +330,41 @@ __global__ void param_check_kernel(const double *__restrict__ m, const double *_
         if (!(b > 0.0 && b <= DBL_MAX))
             atomicMin(&out[1], static_cast<unsigned long long>(i));
     }
+}
+
+// Stream-ordered scratch from a memory pool the library owns, one per device:
+// its release threshold keeps freed blocks for the next call (no re-mapping
+// per call), and -- unlike raising the threshold of the device's DEFAULT pool
+// (round 1) -- it changes nothing for the host application's own
+// cudaMallocAsync users.
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t stream)
+{
+    constexpr int kMaxDev = 64;
+    static cudaMemPool_t pools[kMaxDev] = {};
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess)
+        return e;
+    if (dev < 0 || dev >= kMaxDev)
+        return cudaMallocAsync(p, bytes, stream);
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.handleTypes = cudaMemHandleTypeNone;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if ((e = cudaMemPoolCreate(&pools[dev], &props)) != cudaSuccess)
+                return e;
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = pools[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, stream);
 }
 
 cudaError_t launch_param_check(const double *m, const double *C, int64_t n,

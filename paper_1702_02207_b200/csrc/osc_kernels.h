@@ -99,6 +99,10 @@ cudaError_t launch_energy(const double *m, const double *C, const double *x, con
 cudaError_t launch_first_bad(const int64_t *fb, int64_t B, unsigned long long *out,
                              cudaStream_t stream);
 
+// Stream-ordered scratch from the library's own per-device memory pool
+// (freed with cudaFreeAsync); the device's default pool is left untouched.
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t stream);
+
 // Parameter rule of OscillatorSystem (oscillator.py:75-80): out[0] / out[1]
 // = smallest index of an invalid mass / spring rate (~0 when none).
 // init = false: out[] is already ~0 (staged host calls upload it).

@@ -147,3 +147,33 @@ def test_dense_random_shapes(s, N, nsteps, seed):
     Xo, Vo = oracle.dense_rk4(A, X0, V0, 1e-4, nsteps)
     for got, ref in ((res.x.cpu().numpy(), Xo), (res.v.cpu().numpy(), Vo)):
         assert np.max(np.abs(got - ref)) <= 1e-10 * max(1.0, np.max(np.abs(ref)))
+
+
+@settings(max_examples=60 * _SOAK, deadline=None, derandomize=_DERANDOMIZE,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(B=st.integers(1, 64), s=st.integers(1, 600), seed=st.integers(0, 2**32 - 1),
+       special=st.booleans(), cell_major=st.booleans())
+def test_host_derivative_energy_random(B, s, seed, special, cell_major):
+    """The staged one-round-trip host forms (osc_derivative_host /
+    osc_energy_host, parameter rule fused into the kernels) equal the oracle
+    bit for bit, in both layouts."""
+    import ctypes
+
+    from paper_1702_02207_b200 import _native
+
+    lib = _native.lib()
+    rng = np.random.default_rng(seed)
+    m, C, x0, v0 = _draw_state(rng, (B, s), special)
+    dref = oracle.c_derivative(m, C, x0)
+    eref = oracle.c_energy(m, C, x0, v0)
+    if cell_major:  # [s][B]
+        m, C, x0, v0 = (np.ascontiguousarray(a.T) for a in (m, C, x0, v0))
+    dv = np.empty_like(x0)
+    e = np.empty(B)
+    p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    assert lib.osc_derivative_host(p(m), p(C), p(x0), p(dv), B, s, int(cell_major)) == 0
+    assert lib.osc_energy_host(p(m), p(C), p(x0), p(v0), p(e), B, s, int(cell_major)) == 0
+    got = dv.T if cell_major else dv
+    with np.errstate(all="ignore"):
+        assert bits(np.nan_to_num(got, nan=7.0)) == bits(np.nan_to_num(dref, nan=7.0))
+        assert bits(np.nan_to_num(e, nan=7.0)) == bits(np.nan_to_num(eref, nan=7.0))

@@ -15,6 +15,20 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
                    int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
                    int64_t *first_bad, uint32_t flags, void *stream)
 {
+    return osc_capi::batch2_entry(m, C, x, v, B, dt, nsteps, stride, xs, vs, es, first_bad,
+                                  flags, stream, false);
+}
+
+}  // extern "C"
+
+// osc_rk4_batch2 proper; shares_gpu: the caller runs several batches side
+// by side (the host pipeline's chunks), so K1 keeps its throughput shape
+// even for a small batch.
+int osc_capi::batch2_entry(const double *m, const double *C, double *x, double *v, int64_t B,
+                           double dt, int64_t nsteps, int64_t stride, double *xs, double *vs,
+                           double *es, int64_t *first_bad, uint32_t flags, void *stream,
+                           bool shares_gpu)
+{
     if (flags & ~kRunFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     if (int rc = check_run_args(dt, nsteps, stride))
@@ -31,9 +45,11 @@ int osc_rk4_batch2(const double *m, const double *C, double *x, double *v, int64
             return rc;
     cudaError_t e = osc::launch_batch2(m, C, x, v, B, consts(dt), nsteps, stride, xs, vs, es,
                                        first_bad, (flags & OSC_FMA) != 0,
-                                       static_cast<cudaStream_t>(stream));
+                                       static_cast<cudaStream_t>(stream), nullptr, shares_gpu);
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "batch2_rk4_kernel");
 }
+
+extern "C" {
 
 int osc_rk4_batch2_compare(const double *m, const double *C, double *x, double *v, int64_t B,
                            double dt, int64_t nsteps, int64_t stride, const double *ts,

@@ -227,15 +227,14 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
 
     // -- large: chunked multi-stream pipeline ---------------------------------
     // Chunking, so that only the first chunk's H2D and the last one's D2H are
-    // exposed: >= 2 MB of state per chunk, at most 8 chunks; 2-DOF chunks
-    // keep >= 148*2048 systems so each launch keeps K1's two-systems-per-
-    // thread shape (smaller batches switch to one per thread, which is right
-    // for a lone small batch but 4% slower when chunks run side by side).
+    // exposed: >= 2 MB of state per chunk, at most 8 chunks, 2-DOF chunks of
+    // >= 148*1024 systems; chunks share the GPU, so K1 keeps its two-systems-
+    // per-thread shape for them (batch2_entry's shares_gpu).
     int64_t nchunk = 1;
     if (!xs && B > 1)
         nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 21)}));
     if (!chains)
-        nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 2048)));
+        nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 1024)));
     if (const char *e = std::getenv("OSC_HOST_CHUNKS")) {  // benchmarking knob
         const long long n = std::atoll(e);
         if (!xs && n >= 1 && n <= 64)
@@ -333,8 +332,9 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
             for (int a = 0; a < 2; ++a)
                 for (int r = 0; r < 2; ++r)
                     OSC_CUDA(cudaMemcpyAsync(ds[a] + o + r * nb, hs[a] + r * B + b0, n, H2D, st));
-            if (int rc = osc_rk4_batch2(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride,
-                                        dxs, dvs, nullptr, dfb + b0, OSC_TRUSTED, st))
+            if (int rc = batch2_entry(dm + o, dC + o, dx + o, dv + o, nb, dt, nsteps, stride,
+                                      dxs, dvs, nullptr, dfb + b0, OSC_TRUSTED, st,
+                                      nchunk > 1))
                 return rc;
             OSC_CUDA(cudaEventRecord(evs.ev[nchunk + 1 + c], st));
         }

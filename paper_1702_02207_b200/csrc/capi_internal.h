@@ -317,6 +317,12 @@ inline void edge_sets(const osc::SegArgs &g, int64_t TILE, int64_t nedge[2])
     }
 }
 
+// osc_rk4_batch2 with a shape hint (capi.cu): shares_gpu = the caller runs
+// several batches side by side.
+int batch2_entry(const double *m, const double *C, double *x, double *v, int64_t B, double dt,
+                 int64_t nsteps, int64_t stride, double *xs, double *vs, double *es,
+                 int64_t *first_bad, uint32_t flags, void *stream, bool shares_gpu);
+
 struct Scratch {
     double *p = nullptr;
     cudaStream_t s = nullptr;

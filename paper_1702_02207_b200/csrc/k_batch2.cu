@@ -375,7 +375,7 @@ cudaError_t launch_ns(const double *m, const double *C, double *x, double *v, in
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
                           double *es, int64_t *first_bad, bool fma, cudaStream_t stream,
-                          const CmpArgs *cmp)
+                          const CmpArgs *cmp, bool wide)
 {
     // Launch shape: NS systems per thread x threads per CTA.  OSC_B2="NS,threads"
     // overrides it for benchmarking (read-only process state).
@@ -389,7 +389,7 @@ cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (B < int64_t(sms) * 2048) {
+    if (B < int64_t(sms) * 2048 && !(wide && B >= int64_t(sms) * 256)) {
         ns = 1;
         threads = 128;
     }

@@ -70,10 +70,12 @@ struct CmpArgs {
     double *out;
 };
 
+// wide: keep the two-systems-per-thread throughput shape for small batches
+// too (set when several batches share the GPU side by side).
 cudaError_t launch_batch2(const double *m, const double *C, double *x, double *v, int64_t B,
                           StepConsts k, int64_t nsteps, int64_t stride, double *xs, double *vs,
                           double *es, int64_t *first_bad, bool fma, cudaStream_t stream,
-                          const CmpArgs *cmp = nullptr);
+                          const CmpArgs *cmp = nullptr, bool wide = false);
 
 cudaError_t launch_modal_batch2(const double *m, const double *C, const double *x0,
                                 const double *v0, int64_t B, double *sol, cudaStream_t stream);

@@ -234,7 +234,9 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     if (!xs && B > 1)
         nchunk = std::max<int64_t>(1, std::min<int64_t>({8, B, (int64_t)(bytes >> 21)}));
     if (!chains)
-        nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / (148 * 1024)));
+        // at most 4: measured for C2 (scripts/e2e_chunks.py, profiles/r02):
+        // 2-4 and 8 chunks 49.8-49.9 ms, 6 chunks 53.8 ms
+        nchunk = std::max<int64_t>(1, std::min<int64_t>({nchunk, int64_t(4), B / (148 * 1024)}));
     if (const char *e = std::getenv("OSC_HOST_CHUNKS")) {  // benchmarking knob
         const long long n = std::atoll(e);
         if (!xs && n >= 1 && n <= 64)

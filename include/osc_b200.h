@@ -322,10 +322,24 @@ int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches,
  * osc_device.cuh): 1 = correctly rounded for every numerator the kernels
  * feed it, 2 / 3 = the same with zl moved one ulp toward +inf / -inf, 0 =
  * none.  osc_rk4_batch2 runs the systems whose two masses have a class with
- * it (the chain kernels keep the three-operation division: DESIGN.md).
+ * it (the tiled chain kernels use the checked form, osc_div2c_table).
  * Device buffers;
  * enqueued on `stream`.  Not part of the reference interface (diagnostic). */
 int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream);
+
+/* The checked two-operation division of the chain kernels (osc_device.cuh
+ * div2_checked_consts): zh[i] = RN(1/b[i]), zl[i] = RN(1/b[i] - zh[i]) and
+ * bad[i] = the fraction bits of the one wrong value RN(a*zh + RN(a*zl)) can
+ * take instead of RN(a/b) (it has one failing numerator significand at
+ * most), or 0x9e3779b9 when there is none; the kernels replay a chunk with
+ * IEEE division whenever a quotient's low 32 bits equal bad[i]'s.  zh[i] = 0
+ * marks a divisor that is not
+ * eligible (outside [2^-100, 2^101), or two failing significands): tiles
+ * holding one keep the three-operation division.  osc_rk4_chains computes
+ * this table itself for tiled runs.  Device buffers; enqueued on `stream`.
+ * Not part of the reference interface (diagnostic). */
+int osc_div2c_table(const double *b, int64_t n, double *zh, double *zl, uint64_t *bad,
+                    void *stream);
 
 /* FP64 pipe microbenchmark (roofline denominator; not part of the hot path):
  * enqueues one launch of 8 independent DFMA (mode 0) or DADD (mode 1)

@@ -72,6 +72,7 @@ SIGNATURES = {
     "osc_check_division": (ctypes.c_int, [_i64, ctypes.c_uint64, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_uint64), _vp]),
     "osc_div2_classify": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
+    "osc_div2c_table": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "osc_bench_fp64": (ctypes.c_int, [_i64, ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int64),
                                        _vp]),
     "osc_rk4_batch2_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _dbl, _i64, _i64, _vp,

@@ -391,6 +391,19 @@ def div2_classify(b, *, stream=None) -> torch.Tensor:
     return out.reshape(b.shape)
 
 
+def div2c_table(b, *, stream=None):
+    """(zh, zl, bad) of the chain kernels' checked two-operation division
+    (osc_device.cuh div2_checked_consts; zh == 0: not eligible)."""
+    b = _dev(b)
+    zh = torch.empty(b.numel(), dtype=torch.float64, device=b.device)
+    zl = torch.empty_like(zh)
+    bad = torch.empty(b.numel(), dtype=torch.int64, device=b.device)
+    rc = _native.lib().osc_div2c_table(_ptr(b), b.numel(), _ptr(zh), _ptr(zl), _ptr(bad),
+                                       ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_div2c_table")
+    return zh.reshape(b.shape), zl.reshape(b.shape), bad.reshape(b.shape)
+
+
 # --------------------------------------------------------------------------
 # dense general (M, K) path (BASELINE configs[4]; K5)
 # --------------------------------------------------------------------------

@@ -163,7 +163,25 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     }
     Scratch scratch;
     scratch.s = stream;
-    OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&scratch.p), 2 * bytes, stream));
+    // Tiled runs of the default tile shape divide in two operations where a
+    // tile's divisors allow it (div2_checked_consts): one table pass over the
+    // masses first.  OSC_DIV2=0 keeps three operations (A/B timing).
+    const char *d2env = std::getenv("OSC_DIV2");
+    const bool d2 = !g.fma && (plan.tiles > 1 || plan.H > 0) && K == kTileK &&
+                    threads == kTileThreads && !(d2env && d2env[0] == '0');
+    OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&scratch.p), (d2 ? 5 : 2) * bytes,
+                                stream));
+    if (d2) {
+        double *zh = scratch.p + 2 * cells;
+        g.zh = zh;
+        g.zl = zh + cells;
+        g.bad = reinterpret_cast<const uint64_t *>(zh + 2 * cells);
+        cudaError_t e = osc::launch_div2c_table(m, cells, zh, zh + cells,
+                                                reinterpret_cast<uint64_t *>(zh + 2 * cells),
+                                                stream);
+        if (e != cudaSuccess)
+            return cuda_fail(e, "div2c_table_kernel");
+    }
 
     // The time loop over chains [b0, b0 + nb) on stream st.
     auto run_group = [&](int64_t b0, int64_t nb, cudaStream_t st) -> int {
@@ -171,6 +189,11 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
         osc::SegArgs gg = g;
         gg.m = m + o;
         gg.C = C + o;
+        if (g.zh) {
+            gg.zh = g.zh + o;
+            gg.zl = g.zl + o;
+            gg.bad = g.bad + o;
+        }
         gg.first_bad = first_bad + b0;
         gg.nbuf = nb;
         double *cx = x + o, *cv = v + o, *nx = scratch.p + o, *nv = scratch.p + cells + o;
@@ -497,6 +520,15 @@ int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream)
         return fail(OSC_INVALID, "osc_div2_classify: n < 0 or null buffer");
     cudaError_t e = osc::launch_div2_classify(b, n, pass, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? OSC_OK : cuda_fail(e, "div2_classify_kernel");
+}
+
+int osc_div2c_table(const double *b, int64_t n, double *zh, double *zl, uint64_t *bad,
+                    void *stream)
+{
+    if (n < 0 || (n > 0 && (!b || !zh || !zl || !bad)))
+        return fail(OSC_INVALID, "osc_div2c_table: n < 0 or null buffer");
+    cudaError_t e = osc::launch_div2c_table(b, n, zh, zl, bad, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? OSC_OK : cuda_fail(e, "div2c_table_kernel");
 }
 
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream_)

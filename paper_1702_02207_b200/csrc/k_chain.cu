@@ -34,7 +34,6 @@
 namespace osc {
 namespace {
 
-constexpr int kMaxWarps = 32;
 constexpr int kMaxDevices = 64;
 #ifndef OSC_PERSIST_BUFS
 #define OSC_PERSIST_BUFS 3
@@ -51,45 +50,44 @@ struct Tile {
     int validn;    // cells of this thread inside the tile (pad variant)
     bool first;    // this thread's cell 0 is the tile's first cell (wall side)
     bool last;     // this thread's cell K-1 is the tile's last cell (free side)
-    int lane, warp, nwarps;
 };
 
-// Warp-edge exchange slots, double-buffered by stage parity (compile-time:
-// a step has four stages, so parity restarts at 0 every step).  Slot w+1 of
-// [B][0] holds warp w's first position, of [B][1] its last; slots 0 and
-// nwarps+1 stay 0.0: the first cell then reads x_{-1} = 0.0 and
-// d_0 = x_0 - 0.0 == x_0 exactly (also for x_0 = -0.0), with no select.
+// Thread-edge exchange slots, double-buffered by stage parity (compile-time:
+// a step has four stages, so parity restarts at 0 every step).  Slot t + 1
+// holds thread t's {first, last} stage position; slot 0 stays {0.0, 0.0}:
+// the tile's first cell then reads x_{-1} = 0.0 and d_0 = x_0 - 0.0 == x_0
+// exactly (also for x_0 = -0.0), with no select.  One 16-byte store, one
+// barrier and two 8-byte loads per stage replace the warp shuffles plus the
+// per-warp edge slots of round 1 (the chain kernels are issue-bound: ncu
+// shows their time proportional to instructions issued; 8 -> 3 exchange
+// instructions per stage).
+template <int NT>
 struct Edges {
-    double v[2][2][kMaxWarps + 2];
+    double2 v[2][NT + 2];
 };
 
 // acceleration_at for the K cells of this thread at positions p.  kPad: the
 // tile extends past the buffer end, so cells >= validn are padding whose
 // numerators are replaced by 1.0 (they never feed a real cell: the last real
 // cell has no right neighbour) to keep them off the slow division path.
-template <int K, bool kPad, Arith A, int B>
+template <int K, bool kPad, Arith A, int B, int NT>
 __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], double (&a)[K],
-                                      Edges &e, bool &ok)
+                                      Edges<NT> &e, bool &ok)
 {
-    double pl = __shfl_up_sync(kFull, p[K - 1], 1);
-    double pr = __shfl_down_sync(kFull, p[0], 1);
-    if (t.nwarps > 1) {
-        if (t.lane == 0)
-            e.v[B][0][t.warp + 1] = p[0];
-        if (t.lane == 31)
-            e.v[B][1][t.warp + 1] = p[K - 1];
-        __syncthreads();
-        if (t.lane == 31)
-            pr = e.v[B][0][t.warp + 2];
-    }
-    if (t.lane == 0)
-        pl = e.v[B][1][t.warp];  // left neighbour's last position, or the 0.0 slot
+    e.v[B][threadIdx.x + 1] = make_double2(p[0], p[K - 1]);
+    __syncthreads();
+    const double pl = e.v[B][threadIdx.x].y;      // left neighbour's last, or the 0.0 slot
+    const double pr = e.v[B][threadIdx.x + 2].x;  // right neighbour's first (unused at the end)
     double f[K];
     f[0] = mul(t.C[0], sub(p[0], pl));
 #pragma unroll
     for (int j = 1; j < K; ++j)
         f[j] = mul(t.C[j], sub(p[j], p[j - 1]));
     const double fr = mul(t.Cn, sub(pr, p[K - 1]));
+    // Fast2C: the significand tests accumulate in their own flag, merged once
+    // per stage, so they form a chain of their own beside the quotient tests
+    // instead of doubling the length of one serial predicate chain.
+    bool okb = true;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         double num;
@@ -105,8 +103,13 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
         } else {
             num = sub(t.last ? -0.0 : fr, f[j]);
         }
-        a[j] = qdiv<A>(num, t.md[j], ok);
+        if constexpr (A == Arith::Fast2C)
+            a[j] = div2c_fast2(num, t.md[j], ok, okb);
+        else
+            a[j] = qdiv<A>(num, t.md[j], ok);
     }
+    if constexpr (A == Arith::Fast2C)
+        ok &= okb;
 }
 
 // A buffer whose divergence was recorded in an EARLIER launch (first_bad <=
@@ -231,16 +234,17 @@ __device__ void edge_done(const SegArgs &g, int sides)
 }
 
 // Zero every slot (sentinels included); callers then __syncthreads().
-__device__ __forceinline__ void edges_init(Edges &e)
+template <int NT>
+__device__ __forceinline__ void edges_init(Edges<NT> &e)
 {
-    for (int i = threadIdx.x; i < 2 * 2 * (kMaxWarps + 2); i += blockDim.x)
-        (&e.v[0][0][0])[i] = 0.0;
+    for (int i = threadIdx.x; i < 2 * (NT + 2); i += blockDim.x)
+        (&e.v[0][0])[i] = make_double2(0.0, 0.0);
 }
 
 // One classical RK4 step (oscillator.py:208-231) of the thread's K cells.
-template <int K, bool kPad, Arith A>
+template <int K, bool kPad, Arith A, int NT>
 __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&v)[K],
-                                     const StepConsts &k, Edges &e, bool &ok)
+                                     const StepConsts &k, Edges<NT> &e, bool &ok)
 {
     double a[K], yp[K], yv[K], sx[K], sv[K];
     accel<K, kPad, A, 0>(t, x, a, e, ok);  // k1
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     chain_rk4_kernel(SegArgs g)
 {
     constexpr bool kQ = K * kMaxT == 1024 && K >= 4;
-    __shared__ Edges edges;
+    __shared__ Edges<kMaxT> edges;
     __shared__ int s_skip;
     const int64_t nw = walk_tiles(g);
     const int64_t buf_id = blockIdx.x / nw;
@@ -372,9 +376,6 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     const int64_t c0 = L + static_cast<int64_t>(threadIdx.x) * K;
 
     Tile<K> t;
-    t.lane = threadIdx.x & 31;
-    t.warp = threadIdx.x >> 5;
-    t.nwarps = blockDim.x >> 5;
     t.first = threadIdx.x == 0;
     t.last = threadIdx.x == blockDim.x - 1;
     const int64_t lastc = cend - 1;
@@ -579,7 +580,15 @@ __device__ __forceinline__ TileGeom tile_geom(const SegArgs &g, int64_t it, int6
     return tg;
 }
 
-template <int K, int NT>
+// Shared-memory layout of one tile buffer, in doubles of TILE cells:
+//   three-operation division: [m | C | x | v]
+//   checked two-operation division (kD2): [zh | C | x | v | zl | bad]
+template <bool kD2>
+__host__ __device__ constexpr int64_t tile_slots() { return kD2 ? 6 : 4; }
+template <bool kD2>
+__host__ __device__ constexpr int persist_bufs() { return kD2 ? 2 : kPersistBufs; }
+
+template <int K, int NT, bool kD2>
 __device__ __forceinline__ void issue_tile(const SegArgs &g, int64_t it, double *dst,
                                            uint64_t *bar)
 {
@@ -589,38 +598,44 @@ __device__ __forceinline__ void issue_tile(const SegArgs &g, int64_t it, double 
     if (tg.sides)  // an edge tile reads ghosts the neighbour stores: wait for them
         edge_wait(g.sync, tg.sides);
     const int64_t o = tg.base + tg.L;
-    mbar_expect_tx(bar, 4 * bytes);
-    bulk_g2s(dst, g.m + o, bytes, bar);
+    mbar_expect_tx(bar, tile_slots<kD2>() * bytes);
+    bulk_g2s(dst, (kD2 ? g.zh : g.m) + o, bytes, bar);
     bulk_g2s(dst + TILE, g.C + o, bytes, bar);
     bulk_g2s(dst + 2 * TILE, g.xin + o, bytes, bar);
     bulk_g2s(dst + 3 * TILE, g.vin + o, bytes, bar);
+    if constexpr (kD2) {
+        bulk_g2s(dst + 4 * TILE, g.zl + o, bytes, bar);
+        bulk_g2s(dst + 5 * TILE, g.bad + o, bytes, bar);
+    }
 }
 
-template <int K, int NT, bool kFma>
+template <int K, int NT, bool kFma, bool kD2>
 __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_persistent(SegArgs g)
 {
     constexpr int64_t TILE = int64_t(NT) * K;
-    // kPersistBufs x [m | C | x | v] x TILE.  Three buffers: tile i computes
+    constexpr int kBufs = persist_bufs<kD2>();
+    constexpr int64_t kStride = tile_slots<kD2>() * TILE;  // doubles per tile buffer
+    // kBufs x [m | C | x | v] x TILE (kD2: [zh | C | x | v | zl | bad], two buffers).  Three buffers: tile i computes
     // in buffer i % 3 while tile i + 1's inputs sit loaded in the next one and
     // tile i - 1's results still drain from the third by bulk store, so the
     // refill at the end of tile i (tile i + 2, into the buffer tile i - 1
     // used) waits for a store issued a whole tile earlier, not for the one it
     // just issued.
     extern __shared__ __align__(128) double tbuf[];
-    __shared__ Edges edges;
-    __shared__ __align__(8) uint64_t bars[kPersistBufs];
+    __shared__ Edges<NT> edges;
+    __shared__ __align__(8) uint64_t bars[kBufs];
     __shared__ int s_skip;
 
     const int64_t ntiles = walk_tiles(g) * g.nbuf;
     edges_init(edges);
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kPersistBufs; ++b)
+        for (int b = 0; b < kBufs; ++b)
             mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int b = 0; b < 2; ++b) {
             const int64_t it = blockIdx.x + int64_t(b) * gridDim.x;
             if (it < ntiles)
-                issue_tile<K, NT>(g, it, tbuf + b * 4 * TILE, &bars[b]);
+                issue_tile<K, NT, kD2>(g, it, tbuf + b * kStride, &bars[b]);
         }
         // one buffer: the skip decision is launch-invariant (diverged_before
         // reads the state at launch start), so it is read once, not per tile
@@ -632,17 +647,14 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
     const bool skip_once = g.nbuf == 1 && s_skip != 0;
 
     Tile<K> t;
-    t.lane = threadIdx.x & 31;
-    t.warp = threadIdx.x >> 5;
-    t.nwarps = NT >> 5;
     t.first = threadIdx.x == 0;
     t.last = threadIdx.x == NT - 1;
     t.lastj = -1;
     t.validn = K;
     const int cl = threadIdx.x * K;  // first cell of this thread within the tile
-    int i = 0, b = 0, use = 0;  // b = i % kPersistBufs, use = i / kPersistBufs
+    int i = 0, b = 0, use = 0;  // b = i % kBufs, use = i / kBufs
     for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x, ++i) {
-        double *sm = tbuf + b * 4 * TILE;
+        double *sm = tbuf + b * kStride;
         mbar_wait(&bars[b], use & 1);
         const TileGeom tg = tile_geom(g, it, TILE);
         const int64_t c0 = tg.L + cl;
@@ -655,14 +667,42 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
         }
         if (!skip) {
             bool ok = true;
-            double mj[K];
-            lds_cells<K>(sm + cl, mj);
-            lds_cells<K>(sm + TILE + cl, t.C);
+            bool d2 = false;
+            if constexpr (kD2) {
+                // checked two-operation division iff every divisor of the tile
+                // is eligible (CTA-uniform: the stage barriers couple the CTA)
+                double zh[K], zl[K];
+                lds_cells<K>(sm + cl, zh);
+                bool elig = true;
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                t.md[j] = make_divisor(mj[j]);
-                ok &= kFma ? divisor_fast_ok(t.md[j]) : divisor_range_ok(t.md[j]);
+                for (int j = 0; j < K; ++j)
+                    elig &= zh[j] != 0.0;
+                d2 = __syncthreads_and(elig) != 0;
+                if (d2) {
+                    lds_cells<K>(sm + 4 * TILE + cl, zl);
+                    const uint64_t *bw = reinterpret_cast<const uint64_t *>(sm + 5 * TILE) + cl;
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+                        t.md[j] = Divisor{0.0, zh[j], zl[j], static_cast<uint32_t>(bw[j])};
+                } else {
+                    // an ineligible divisor: the three-operation loop, masses
+                    // from global memory (they are not in the tile buffer)
+#pragma unroll
+                    for (int j = 0; j < K; ++j) {
+                        t.md[j] = make_divisor(g.m[tg.base + c0 + j]);
+                        ok &= kFma ? divisor_fast_ok(t.md[j]) : divisor_range_ok(t.md[j]);
+                    }
+                }
+            } else {
+                double mj[K];
+                lds_cells<K>(sm + cl, mj);
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    t.md[j] = make_divisor(mj[j]);
+                    ok &= kFma ? divisor_fast_ok(t.md[j]) : divisor_range_ok(t.md[j]);
+                }
             }
+            lds_cells<K>(sm + TILE + cl, t.C);
             t.Cn = (cl + K < TILE) ? sm[TILE + cl + K] : 1.0;
             double x[K], v[K];
             lds_cells<K>(sm + 2 * TILE + cl, x);
@@ -670,12 +710,28 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             // single-test division here (div_fastq): -5% instructions, C3
             // +1.1%; the whole-chain kernel keeps div_fast, whose schedule
             // ptxas handles better (profiles/r01/README.md)
-            for (int64_t s = 0; s < g.nsteps; ++s)
-                step<K, false, kFma ? Arith::Fma : Arith::FastQ>(t, x, v, g.k, edges, ok);
+#ifdef OSC_EXP_D2_NOFALLBACK  // timing experiment: ineligible tiles go straight to the replay
+            if (kD2 && !d2)
+                ok = false;
+            else if (kD2) {
+#else
+            if (kD2 && d2) {
+#endif
+                for (int64_t s = 0; s < g.nsteps; ++s)
+                    step<K, false, Arith::Fast2C>(t, x, v, g.k, edges, ok);
+            } else {
+                for (int64_t s = 0; s < g.nsteps; ++s)
+                    step<K, false, kFma ? Arith::Fma : Arith::FastQ>(t, x, v, g.k, edges, ok);
+            }
             if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
                 // exact replay from the tile input still in shared memory
                 lds_cells<K>(sm + 2 * TILE + cl, x);
                 lds_cells<K>(sm + 3 * TILE + cl, v);
+                if (kD2 && d2) {
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+                        t.md[j].b = g.m[tg.base + c0 + j];
+                }
                 for (int64_t s = 0; s < g.nsteps; ++s) {
                     step<K, false, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, edges, ok);
                     if (__syncthreads_or(owned_bad<K>(x, v, c0, tg.own_start, tg.own_end))) {
@@ -724,16 +780,16 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 // tile i + 2 goes into the buffer tile i - 1 used: its store
                 // group must have finished reading it (the group just
                 // committed for tile i may stay in flight)
-                if (stored && kPersistBufs == 3)
+                if (stored && kBufs == 3)
                     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 else
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                const int nb = kPersistBufs == 2 ? b : (b == 0 ? kPersistBufs - 1 : b - 1);
+                const int nb = kBufs == 2 ? b : (b == 0 ? kBufs - 1 : b - 1);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_tile<K, NT>(g, nx, tbuf + nb * 4 * TILE, &bars[nb]);
+                issue_tile<K, NT, kD2>(g, nx, tbuf + nb * kStride, &bars[nb]);
             }
         }
-        if (++b == kPersistBufs) {
+        if (++b == kBufs) {
             b = 0;
             ++use;
         }
@@ -742,13 +798,16 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes performed
 }
 
-template <int K, int NT>
-constexpr size_t persist_smem() { return kPersistBufs * 4 * size_t(K) * NT * sizeof(double); }
+template <int K, int NT, bool kD2>
+constexpr size_t persist_smem()
+{
+    return persist_bufs<kD2>() * tile_slots<kD2>() * size_t(K) * NT * sizeof(double);
+}
 
 // Resident CTAs of a persistent kernel on device `dev` (SMs x CTAs per SM),
 // computed once per kernel and device: the attribute call and the occupancy
 // query cost more host time than a short sharded period's launch itself.
-template <int K, int NT, bool kFma>
+template <int K, int NT, bool kFma, bool kD2>
 int64_t persistent_ctas(int dev)
 {
     static std::atomic<int64_t> cache[kMaxDevices];  // one per kernel instantiation
@@ -757,30 +816,42 @@ int64_t persistent_ctas(int dev)
         if (c > 0)
             return c;
     }
-    auto kern = chain_tiles_persistent<K, NT, kFma>;
+    auto kern = chain_tiles_persistent<K, NT, kFma, kD2>;
     int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(persist_smem<K, NT>()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, persist_smem<K, NT>());
+                         static_cast<int>(persist_smem<K, NT, kD2>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, persist_smem<K, NT, kD2>());
     const int64_t c = int64_t(sms) * std::max(per_sm, 1);
     if (dev >= 0 && dev < kMaxDevices)
         cache[dev].store(c, std::memory_order_relaxed);
     return c;
 }
 
-template <int K, int NT>
-cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
+template <int K, int NT, bool kFma, bool kD2>
+cudaError_t launch_persistent_as(const SegArgs &g, cudaStream_t stream)
 {
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = g.fma ? chain_tiles_persistent<K, NT, true> : chain_tiles_persistent<K, NT, false>;
-    const int64_t ctas = g.fma ? persistent_ctas<K, NT, true>(dev)
-                               : persistent_ctas<K, NT, false>(dev);
+    const int64_t ctas = persistent_ctas<K, NT, kFma, kD2>(dev);
     const int64_t ntiles = walk_tiles(g) * g.nbuf;
     const int64_t grid = std::min<int64_t>(ntiles, ctas);
-    kern<<<static_cast<unsigned>(grid), NT, persist_smem<K, NT>(), stream>>>(g);
+    chain_tiles_persistent<K, NT, kFma, kD2>
+        <<<static_cast<unsigned>(grid), NT, persist_smem<K, NT, kD2>(), stream>>>(g);
     return cudaGetLastError();
+}
+
+template <int K, int NT>
+cudaError_t launch_persistent(const SegArgs &g, cudaStream_t stream)
+{
+    if (g.fma)
+        return launch_persistent_as<K, NT, true, false>(g, stream);
+    // the checked two-operation build for the default tile shape only
+    if constexpr (K == 8 && NT == 256) {
+        if (g.zh)
+            return launch_persistent_as<K, NT, false, true>(g, stream);
+    }
+    return launch_persistent_as<K, NT, false, false>(g, stream);
 }
 
 template <int K>
@@ -826,7 +897,8 @@ cudaError_t launch_chain(const SegArgs &g, int K, int threads, cudaStream_t stre
     const bool aligned = (g.n % 2 == 0) && (g.own_lo % 2 == 0) && (g.own_hi % 2 == 0) &&
                          (g.W % 2 == 0) && (g.H % 2 == 0) && g.n >= TILE && a16(g.m) &&
                          a16(g.C) && a16(g.xin) && a16(g.vin) && a16(g.xout) && a16(g.vout) &&
-                         (!g.xs || (a16(g.xs) && a16(g.vs)));
+                         (!g.xs || (a16(g.xs) && a16(g.vs))) &&
+                         (!g.zh || (a16(g.zh) && a16(g.zl) && a16(g.bad)));
     static const bool disable = std::getenv("OSC_NO_PERSIST") != nullptr;
     if (tiled && aligned && !disable) {
         if (K == 8 && threads == 128)

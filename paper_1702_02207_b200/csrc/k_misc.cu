@@ -89,6 +89,12 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t z)
 //   mode 4: div2_fast on numerators next to quotient midpoints (see below)
 //   mode 5: div_fastq with its flag (divisor_range_ok, quotient_fast_ok), b any
 //           positive double, a any pattern
+//   mode 6: the checked two-operation division (div2c_fast, div2_checked_consts
+//           -- the chain kernels' Fast2C) with its flag, b and a as mode 5
+//   mode 7: div2c_fast on mode 4's midpoint-aimed numerators
+//   mode 8: as mode 7, but counts the WRONG two-operation quotients that the
+//           flag caught (evidence that the aimed numerators hit the failing
+//           significands the check exists for)
 __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                                       unsigned long long *mismatches)
 {
@@ -99,7 +105,7 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
         const uint64_t r2 = splitmix(seed ^ (2 * static_cast<uint64_t>(i) + 1));
         const uint64_t mant_b = r2 & 0x000fffffffffffffull;
         uint64_t bb;
-        if (mode == 1 || (mode == 5 && ((r1 >> 11) & 1))) {
+        if (mode == 1 || ((mode == 5 || mode == 6) && ((r1 >> 11) & 1))) {
             uint64_t e = (r2 >> 52) & 0x7ff;
             if (e == 0x7ff)
                 e = 0x7fe;
@@ -129,6 +135,19 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                 ++bad;
             continue;
         }
+        if (mode == 6) {
+            const double a = __longlong_as_double(static_cast<long long>(ab));
+            const double b = __longlong_as_double(static_cast<long long>(bb));
+            double zh, zl;
+            uint64_t w;
+            if (!div2_checked_consts(b, zh, zl, w))
+                continue;
+            bool ok = true;
+            const double got = div2c_fast(a, Divisor{b, zh, zl, static_cast<uint32_t>(w)}, ok);
+            if (ok && __double_as_longlong(got) != __double_as_longlong(__ddiv_rn(a, b)))
+                ++bad;
+            continue;
+        }
         if (mode >= 3) {
             // The two-operation division (div2_fast) on divisors that pass
             // div2_classify; mode 4 aims every numerator at a rounding
@@ -136,7 +155,7 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
             // k and binade (sh = 53: a/b >= 1, sh = 54: a/b < 1), and scales
             // a and b by random powers of two inside the admissible ranges.
             double b0 = __longlong_as_double(static_cast<long long>(bb));
-            if (mode == 4) {
+            if (mode == 4 || mode >= 7) {
                 const uint64_t B = mant_b | (1ull << 52);
                 const uint64_t Bo = B >> (__ffsll(static_cast<long long>(B)) - 1);
                 const int sh = (r1 & 1) ? 53 : 54;
@@ -158,6 +177,21 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                      (A & 0x000fffffffffffffull);
                 b0 = __longlong_as_double(static_cast<long long>(
                     (uint64_t(1023 + eb) << 52) | mant_b));
+            }
+            if (mode >= 7) {
+                double zh, zl;
+                uint64_t w;
+                if (!div2_checked_consts(b0, zh, zl, w))
+                    continue;
+                const double a = __longlong_as_double(static_cast<long long>(ab));
+                bool ok = true;
+                const double got =
+                    div2c_fast(a, Divisor{b0, zh, zl, static_cast<uint32_t>(w)}, ok);
+                const bool wrong =
+                    __double_as_longlong(got) != __double_as_longlong(__ddiv_rn(a, b0));
+                if (mode == 7 ? (ok && wrong) : (!ok && wrong))
+                    ++bad;
+                continue;
             }
             double zh, zl;
             const int cls = div2_classify(b0, zh, zl);
@@ -467,6 +501,31 @@ cudaError_t launch_div2_classify(const double *b, int64_t n, uint8_t *pass, cuda
     const int64_t want = (n + 255) / 256;
     div2_classify_kernel<<<static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16), 256, 0,
                            stream>>>(b, n, pass);
+    return cudaGetLastError();
+}
+
+__global__ void div2c_table_kernel(const double *__restrict__ b, int64_t n, double *__restrict__ zh,
+                                   double *__restrict__ zl, uint64_t *__restrict__ bad)
+{
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double h, l;
+        uint64_t w;
+        div2_checked_consts(b[i], h, l, w);
+        zh[i] = h;
+        zl[i] = l;
+        bad[i] = w;
+    }
+}
+
+cudaError_t launch_div2c_table(const double *b, int64_t n, double *zh, double *zl, uint64_t *bad,
+                               cudaStream_t stream)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const int64_t want = (n + 255) / 256;
+    div2c_table_kernel<<<static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16), 256, 0,
+                         stream>>>(b, n, zh, zl, bad);
     return cudaGetLastError();
 }
 

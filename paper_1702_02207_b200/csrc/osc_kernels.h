@@ -53,6 +53,12 @@ struct SegArgs {
     bool ordered;
     int64_t nedge[2];
     int64_t walk0, nwalk;
+    // Checked two-operation division (div2_checked_consts) of every cell,
+    // [nbuf][n] like m; zh == 0 marks an ineligible divisor, bad holds the
+    // tested low word in 8-byte slots (bulk-copy alignment).  Null: the
+    // three-operation division.
+    const double *zh, *zl;
+    const uint64_t *bad;
 };
 
 // Tiles one buffer's launch walks.
@@ -110,6 +116,10 @@ cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t stream);
 // init = false: out[] is already ~0 (staged host calls upload it).
 cudaError_t launch_param_check(const double *m, const double *C, int64_t n,
                                unsigned long long *out, cudaStream_t stream, bool init = true);
+
+// zh, zl, bad of div2_checked_consts for n divisors (SegArgs::zh/zl/bad).
+cudaError_t launch_div2c_table(const double *b, int64_t n, double *zh, double *zl, uint64_t *bad,
+                               cudaStream_t stream);
 
 cudaError_t launch_div2_classify(const double *b, int64_t n, uint8_t *pass, cudaStream_t stream);
 

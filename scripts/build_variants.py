@@ -17,6 +17,11 @@ VARIANTS = {
     "u2": ["-DOSC_B2_UNROLL=2"],
     "u8": ["-DOSC_B2_UNROLL=8"],
     "pb2": ["-DOSC_PERSIST_BUFS=2"],  # K3 double-buffered (round 1) vs 3 buffers
+    # K3 checked two-operation division: timing-only experiments (d2nc is NOT exact)
+    "d2nc": ["-DOSC_EXP_D2_NOCHECK"],
+    "d2nf": ["-DOSC_EXP_D2_NOFALLBACK"],
+    "d2a": ["-DOSC_EXP_D2_CHECKA"],
+    "d2anf": ["-DOSC_EXP_D2_CHECKA", "-DOSC_EXP_D2_NOFALLBACK"],
 }
 
 if __name__ == "__main__":

@@ -13,6 +13,7 @@ a/b < 1); 0 = none.
 from __future__ import annotations
 
 import math
+import struct
 from fractions import Fraction
 
 
@@ -75,3 +76,34 @@ def classify(b: float) -> int:
         if all(div2(A / 2 ** 52, zh, z) == (A / 2 ** 52) / bs for _, _, A in cands):
             return cls
     return 0
+
+
+NO_BAD = 0x9E3779B9  # kDiv2NoBad: the tested low word of a divisor with no failure
+
+
+def checked_consts(b: float):
+    """div2_checked_consts (osc_device.cuh), the chain kernels' checked
+    two-operation division: (zh, zl, bad) with class-1 constants in b's own
+    binade and ``bad`` the fraction bits of the wrong two-operation quotient
+    of the one failing candidate significand (NO_BAD when none), or None when
+    b is not eligible (outside [2^-100, 2^101), |zl| < 2^-80 zh, or two
+    failures)."""
+    if not (2.0 ** -100 <= b < 2.0 ** 101):
+        return None
+    B, e = significand(b)
+    bs = B / 2 ** 52
+    zh, zl = consts(bs)
+    scale = 2.0 ** -e
+    if B == 2 ** 52:
+        return zh * scale, 0.0, NO_BAD
+    if abs(zl) < 2.0 ** -80 * zh:
+        return None
+    fails = [A for _, _, A in candidates(b) if div2(A / 2 ** 52, zh, zl) != (A / 2 ** 52) / bs]
+    if len(fails) > 1:
+        return None
+    bad = fraction_bits(div2(fails[0] / 2 ** 52, zh, zl)) if fails else NO_BAD
+    return zh * scale, zl * scale, bad
+
+
+def fraction_bits(a: float) -> int:
+    return struct.unpack("<Q", struct.pack("<d", a))[0] & (2 ** 52 - 1)

@@ -120,3 +120,65 @@ def test_device_candidate_walk_equals_gcd_solution():
         B = (B | 1, B & ~1, B & ~3, B & ~7)[i % 4] | (1 << 52)
         want = sorted(A for _, _, A in dm.candidates(B / 2 ** 52))
         assert _device_enumeration(B) == want, B
+
+
+# ---------------------------------------------------------------------------
+# The checked form of the chain kernels (div2_checked_consts / div2c_fast):
+# class-1 constants for every divisor, and a per-division test of the one
+# significand that can round wrongly.
+# ---------------------------------------------------------------------------
+
+def test_checked_form_fails_only_at_the_stored_significand():
+    """Numerators aimed at midpoints from |k| <= 12: a wrong two-operation
+    quotient only ever comes from the one failing significand and equals the
+    stored wrong quotient, so the kernels' low-word test catches every one."""
+    rng = random.Random(20261020)
+    caught = 0
+    for _ in range(1500):
+        b = rng.uniform(1.0, 2.0)
+        cc = dm.checked_consts(b)
+        assert cc is not None, b
+        zh, zl, bad = cc
+        for sh, k, A in dm.candidates(b, kmax53=12, kmax54=12):
+            x = A / 2 ** 52
+            q = dm.div2(x, zh, zl)
+            if q != x / b:
+                assert dm.fraction_bits(q) == bad, (b, sh, k, A)
+                assert (bad & 0xFFFFFFFF) != dm.NO_BAD
+                caught += 1
+    assert caught > 5  # the aimed numerators do hit failing significands
+
+
+def test_checked_form_eligibility_and_scaling():
+    rng = random.Random(4)
+    n_fail = n_inel = 0
+    for _ in range(20000):
+        b = rng.uniform(0.5, 2.0)
+        cc = dm.checked_consts(b)
+        if cc is None:
+            n_inel += 1
+            continue
+        n_fail += (cc[2] & 0xFFFFFFFF) != dm.NO_BAD
+    assert n_inel == 0  # every random mass is eligible (two failures: none seen)
+    assert 0.005 < n_fail / 20000 < 0.03  # ~1.2% carry one failing significand
+    for b in (1.0, 0.5, 2.0, 2.0 ** 100, 2.0 ** -100):
+        assert dm.checked_consts(b)[1:] == (0.0, dm.NO_BAD)
+    for b in (2.0 ** 101, 2.0 ** -101, 0.0, -1.0, float("inf")):
+        assert dm.checked_consts(b) is None
+    # scaled divisors, numerators in many binades: exact, or flagged -- also
+    # the failing significand itself, scaled (the wrong quotient scales too)
+    for _ in range(300):
+        b = rng.uniform(0.5, 2.0) * 2.0 ** rng.randint(-90, 90)
+        zh, zl, bad = dm.checked_consts(b)
+        B, _ = dm.significand(b)
+        bs = B / 2 ** 52
+        hs, ls = dm.consts(bs)
+        fails = [A for _, _, A in dm.candidates(b) if dm.div2(A / 2 ** 52, hs, ls) != (A / 2 ** 52) / bs]
+        nums = [rng.uniform(-4.0, 4.0) * 2.0 ** rng.randint(-40, 40) for _ in range(50)]
+        nums += [A / 2 ** 52 * 2.0 ** rng.randint(-40, 40) * rng.choice((1, -1)) for A in fails]
+        for a in nums:
+            q = dm.div2(a, zh, zl)
+            if (dm.fraction_bits(q) & 0xFFFFFFFF) != (bad & 0xFFFFFFFF):
+                assert q == a / b, (a, b)
+            elif a in nums[50:]:
+                assert q != a / b  # the failing numerator really is caught

@@ -38,7 +38,14 @@ constexpr int kMaxDevices = 64;
 #ifndef OSC_PERSIST_BUFS
 #define OSC_PERSIST_BUFS 3
 #endif
-constexpr int kPersistBufs = OSC_PERSIST_BUFS;  // tile buffers of the persistent kernel (see there)
+constexpr int kPersistBufs = OSC_PERSIST_BUFS;
+#ifndef OSC_CHAIN_UNROLL
+#define OSC_CHAIN_UNROLL 1
+#endif
+constexpr int kChainUnroll = OSC_CHAIN_UNROLL;  // K3 step-loop unroll (timing experiments)
+#ifndef OSC_D2_CHOICE
+#define OSC_D2_CHOICE 2
+#endif  // tile buffers of the persistent kernel (see there)
 static_assert(kPersistBufs == 2 || kPersistBufs == 3, "2 or 3 tile buffers");
 
 template <int K>
@@ -50,6 +57,8 @@ struct Tile {
     int validn;    // cells of this thread inside the tile (pad variant)
     bool first;    // this thread's cell 0 is the tile's first cell (wall side)
     bool last;     // this thread's cell K-1 is the tile's last cell (free side)
+    int pr_off;    // byte offset in a stage's slot row of the value read as the right neighbour
+    bool tested;   // Fast2T: this warp holds a divisor whose quotients are tested (warp-uniform)
 };
 
 // Thread-edge exchange slots, double-buffered by stage parity (compile-time:
@@ -77,7 +86,11 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
     e.v[B][threadIdx.x + 1] = make_double2(p[0], p[K - 1]);
     __syncthreads();
     const double pl = e.v[B][threadIdx.x].y;      // left neighbour's last, or the 0.0 slot
-    const double pr = e.v[B][threadIdx.x + 2].x;  // right neighbour's first (unused at the end)
+    // right neighbour's first position; the last thread reads its own last
+    // one (t.pr_off), so that with t.Cn = -0.0 its fr is exactly -0.0 and
+    // the free end's numerator (-0.0) - f needs no select (see below)
+    const double pr = *reinterpret_cast<const double *>(
+        reinterpret_cast<const char *>(&e.v[B][0]) + t.pr_off);
     double f[K];
     f[0] = mul(t.C[0], sub(p[0], pl));
 #pragma unroll
@@ -100,8 +113,14 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
             num = (j < t.validn) ? num : 1.0;
         } else if (j + 1 < K) {
             num = sub(f[j + 1], f[j]);
-        } else {
+        } else if constexpr (A == Arith::Exact) {
             num = sub(t.last ? -0.0 : fr, f[j]);
+        } else {
+            // The last thread's fr = (-0.0)*(p - p) is -0.0 for a finite p,
+            // so this is (-0.0) - f bit for bit.  A non-finite p makes the
+            // cell non-finite in the reference too: the chunk is replayed
+            // with the literal select above.
+            num = sub(fr, f[j]);
         }
         if constexpr (A == Arith::Fast2C)
             a[j] = div2c_fast2(num, t.md[j], ok, okb);
@@ -110,6 +129,14 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
     }
     if constexpr (A == Arith::Fast2C)
         ok &= okb;
+    if constexpr (A == Arith::Fast2T) {
+        if (t.tested) {  // warp-uniform: 12% of C3's warps
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                okb &= static_cast<uint32_t>(__double2loint(a[j])) != t.md[j].bad;
+            ok &= okb;
+        }
+    }
 }
 
 // A buffer whose divergence was recorded in an EARLIER launch (first_bad <=
@@ -247,6 +274,11 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
                                      const StepConsts &k, Edges<NT> &e, bool &ok)
 {
     double a[K], yp[K], yv[K], sx[K], sv[K];
+    if constexpr (A != Arith::Exact && A != Arith::Fma) {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            ok &= velocity_small(v[j]);  // add_twice_fused's condition
+    }
     accel<K, kPad, A, 0>(t, x, a, e, ok);  // k1
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -258,7 +290,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
     accel<K, kPad, A, 1>(t, yp, a, e, ok);  // k2
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        sx[j] = add_twice_checked<A>(sx[j], yv[j], ok);
+        sx[j] = add_twice_fused<A>(sx[j], yv[j]);
         sv[j] = add_twice<A>(sv[j], a[j]);
         yp[j] = stage<A>(x[j], k.half_dt, yv[j]);
         yv[j] = stage<A>(v[j], k.half_dt, a[j]);
@@ -266,7 +298,7 @@ __device__ __forceinline__ void step(const Tile<K> &t, double (&x)[K], double (&
     accel<K, kPad, A, 0>(t, yp, a, e, ok);  // k3
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        sx[j] = add_twice_checked<A>(sx[j], yv[j], ok);
+        sx[j] = add_twice_fused<A>(sx[j], yv[j]);
         sv[j] = add_twice<A>(sv[j], a[j]);
         yp[j] = stage<A>(x[j], k.dt, yv[j]);
         yv[j] = stage<A>(v[j], k.dt, a[j]);
@@ -378,6 +410,8 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     Tile<K> t;
     t.first = threadIdx.x == 0;
     t.last = threadIdx.x == blockDim.x - 1;
+    t.pr_off = t.last ? static_cast<int>((threadIdx.x + 1) * sizeof(double2) + sizeof(double))
+                      : static_cast<int>((threadIdx.x + 2) * sizeof(double2));
     const int64_t lastc = cend - 1;
     t.lastj = (lastc >= c0 && lastc < c0 + K) ? static_cast<int>(lastc - c0) : -1;
     t.validn = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(K),
@@ -390,11 +424,11 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
         t.md[j] = make_divisor(c < cend ? g.m[base + c] : 1.0);
         ok0 &= (kQ && !kFma) ? divisor_range_ok(t.md[j]) : divisor_fast_ok(t.md[j]);
     }
-    t.Cn = (c0 + K < cend) ? g.C[base + c0 + K] : 1.0;
+    t.Cn = (c0 + K < cend) ? g.C[base + c0 + K] : (t.last ? -0.0 : 1.0);
 
     double x[K], v[K];
     load_state<K>(g, base, c0, cend, x, v);
-    bool ok = ok0;
+    bool ok = ok0 && fused_dt_ok(g.k.half_dt);
     for (int64_t s = 0; s < g.nsteps; ++s)
         step<K, kPad, kFma ? Arith::Fma : (kQ ? Arith::FastQ : Arith::Fast)>(t, x, v, g.k, edges, ok);
 
@@ -649,7 +683,10 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
     Tile<K> t;
     t.first = threadIdx.x == 0;
     t.last = threadIdx.x == NT - 1;
+    t.pr_off = t.last ? static_cast<int>((threadIdx.x + 1) * sizeof(double2) + sizeof(double))
+                      : static_cast<int>((threadIdx.x + 2) * sizeof(double2));
     t.lastj = -1;
+    t.tested = false;
     t.validn = K;
     const int cl = threadIdx.x * K;  // first cell of this thread within the tile
     int i = 0, b = 0, use = 0;  // b = i % kBufs, use = i / kBufs
@@ -666,32 +703,43 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             skip = s_skip != 0;
         }
         if (!skip) {
-            bool ok = true;
-            bool d2 = false;
+            bool ok = fused_dt_ok(g.k.half_dt);
+            // kD2: 2 = this warp divides in two operations without tests (all
+            // its divisors have a class), 1 = with the wrong-quotient tests,
+            // 0 = a divisor of the tile is not eligible: straight to the
+            // exact replay (masses outside [2^-100, 2^101); none in C3)
+            int d2 = 0;
             if constexpr (kD2) {
-                // checked two-operation division iff every divisor of the tile
-                // is eligible (CTA-uniform: the stage barriers couple the CTA)
                 double zh[K], zl[K];
                 lds_cells<K>(sm + cl, zh);
                 bool elig = true;
 #pragma unroll
                 for (int j = 0; j < K; ++j)
                     elig &= zh[j] != 0.0;
-                d2 = __syncthreads_and(elig) != 0;
-                if (d2) {
+                if (__syncthreads_and(elig)) {
                     lds_cells<K>(sm + 4 * TILE + cl, zl);
                     const uint64_t *bw = reinterpret_cast<const uint64_t *>(sm + 5 * TILE) + cl;
-#pragma unroll
-                    for (int j = 0; j < K; ++j)
-                        t.md[j] = Divisor{0.0, zh[j], zl[j], static_cast<uint32_t>(bw[j])};
-                } else {
-                    // an ineligible divisor: the three-operation loop, masses
-                    // from global memory (they are not in the tile buffer)
+                    bool clean = true;
 #pragma unroll
                     for (int j = 0; j < K; ++j) {
-                        t.md[j] = make_divisor(g.m[tg.base + c0 + j]);
-                        ok &= kFma ? divisor_fast_ok(t.md[j]) : divisor_range_ok(t.md[j]);
+                        const uint64_t w = bw[j];
+                        t.md[j] = Divisor{0.0, zh[j], zl[j], static_cast<uint32_t>(w)};
+                        clean &= (w & kDiv2Clean) != 0;
                     }
+#if OSC_D2_CHOICE == 0
+                    d2 = 1;
+#elif OSC_D2_CHOICE == 1
+                    d2 = __syncthreads_and(clean) ? 2 : 1;
+#elif OSC_D2_CHOICE == 3  // timing bound only: NOT exact
+                    d2 = 2;
+#elif OSC_D2_CHOICE == 4
+                    t.tested = __any_sync(kFull, !clean);
+                    d2 = 3;
+#else
+                    d2 = __all_sync(kFull, clean) ? 2 : 1;
+#endif
+                } else {
+                    ok = false;
                 }
             } else {
                 double mj[K];
@@ -703,23 +751,27 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 }
             }
             lds_cells<K>(sm + TILE + cl, t.C);
-            t.Cn = (cl + K < TILE) ? sm[TILE + cl + K] : 1.0;
+            t.Cn = (cl + K < TILE) ? sm[TILE + cl + K] : -0.0;  // -0.0: the free end (accel)
             double x[K], v[K];
             lds_cells<K>(sm + 2 * TILE + cl, x);
             lds_cells<K>(sm + 3 * TILE + cl, v);
             // single-test division here (div_fastq): -5% instructions, C3
             // +1.1%; the whole-chain kernel keeps div_fast, whose schedule
             // ptxas handles better (profiles/r01/README.md)
-#ifdef OSC_EXP_D2_NOFALLBACK  // timing experiment: ineligible tiles go straight to the replay
-            if (kD2 && !d2)
-                ok = false;
-            else if (kD2) {
-#else
-            if (kD2 && d2) {
-#endif
-                for (int64_t s = 0; s < g.nsteps; ++s)
-                    step<K, false, Arith::Fast2C>(t, x, v, g.k, edges, ok);
+            if constexpr (kD2) {
+                // warp-uniform choice; both loops pass the same barriers
+                if (d2 == 3) {
+                    for (int64_t s = 0; s < g.nsteps; ++s)
+                        step<K, false, Arith::Fast2T>(t, x, v, g.k, edges, ok);
+                } else if (d2 == 2) {
+                    for (int64_t s = 0; s < g.nsteps; ++s)
+                        step<K, false, Arith::Fast2>(t, x, v, g.k, edges, ok);
+                } else if (d2 == 1) {
+                    for (int64_t s = 0; s < g.nsteps; ++s)
+                        step<K, false, Arith::Fast2C>(t, x, v, g.k, edges, ok);
+                }
             } else {
+#pragma unroll kChainUnroll
                 for (int64_t s = 0; s < g.nsteps; ++s)
                     step<K, false, kFma ? Arith::Fma : Arith::FastQ>(t, x, v, g.k, edges, ok);
             }
@@ -727,7 +779,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                 // exact replay from the tile input still in shared memory
                 lds_cells<K>(sm + 2 * TILE + cl, x);
                 lds_cells<K>(sm + 3 * TILE + cl, v);
-                if (kD2 && d2) {
+                if (kD2) {  // the masses are not in the tile buffer
 #pragma unroll
                     for (int j = 0; j < K; ++j)
                         t.md[j].b = g.m[tg.base + c0 + j];

@@ -511,7 +511,7 @@ __global__ void div2c_table_kernel(const double *__restrict__ b, int64_t n, doub
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double h, l;
         uint64_t w;
-        div2_checked_consts(b[i], h, l, w);
+        div2_chain_consts(b[i], h, l, w);
         zh[i] = h;
         zl[i] = l;
         bad[i] = w;

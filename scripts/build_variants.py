@@ -17,11 +17,13 @@ VARIANTS = {
     "u2": ["-DOSC_B2_UNROLL=2"],
     "u8": ["-DOSC_B2_UNROLL=8"],
     "pb2": ["-DOSC_PERSIST_BUFS=2"],  # K3 double-buffered (round 1) vs 3 buffers
-    # K3 checked two-operation division: timing-only experiments (d2nc is NOT exact)
-    "d2nc": ["-DOSC_EXP_D2_NOCHECK"],
-    "d2nf": ["-DOSC_EXP_D2_NOFALLBACK"],
-    "d2a": ["-DOSC_EXP_D2_CHECKA"],
-    "d2anf": ["-DOSC_EXP_D2_CHECKA", "-DOSC_EXP_D2_NOFALLBACK"],
+    # K3 two-operation loop choice: 0 all tested, 1 per tile, 2 per warp
+    "d2c0": ["-DOSC_D2_CHOICE=0"],
+    "d2c1": ["-DOSC_D2_CHOICE=1"],
+    "d2c3": ["-DOSC_D2_CHOICE=3"],
+    "d2c4": ["-DOSC_D2_CHOICE=4"],
+    "cu2": ["-DOSC_CHAIN_UNROLL=2"],  # timing bound only: never tested quotients (NOT exact)
+
 }
 
 if __name__ == "__main__":

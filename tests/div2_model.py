@@ -107,3 +107,17 @@ def checked_consts(b: float):
 
 def fraction_bits(a: float) -> int:
     return struct.unpack("<Q", struct.pack("<d", a))[0] & (2 ** 52 - 1)
+
+
+CLEAN = 1 << 63  # kDiv2Clean: a divisor whose quotients need no test
+
+
+def chain_consts(b: float):
+    """div2_chain_consts (osc_device.cuh), the chain kernels' table entry: a
+    divisor with a class gets that class's constants and ``CLEAN | NO_BAD``;
+    any other divisor the checked form's (checked_consts), or None."""
+    cls = classify(b)
+    if cls:
+        zh, zl = consts(b)
+        return zh, class_zl(zl, cls), CLEAN | NO_BAD
+    return checked_consts(b)

@@ -182,3 +182,22 @@ def test_checked_form_eligibility_and_scaling():
                 assert q == a / b, (a, b)
             elif a in nums[50:]:
                 assert q != a / b  # the failing numerator really is caught
+
+
+def test_chain_table_entries():
+    """div2_chain_consts: classed divisors keep their class constants and need
+    no test; the rest carry the checked form's wrong quotient."""
+    rng = random.Random(8)
+    kinds = {"clean": 0, "checked": 0}
+    for _ in range(6000):
+        b = rng.uniform(0.5, 2.0)
+        zh, zl, bad = dm.chain_consts(b)
+        cls = dm.classify(b)
+        if cls:
+            assert bad == dm.CLEAN | dm.NO_BAD
+            assert (zh, zl) == (dm.consts(b)[0], dm.class_zl(dm.consts(b)[1], cls))
+            kinds["clean"] += 1
+        else:
+            assert not bad & dm.CLEAN and (zh, zl, bad) == dm.checked_consts(b)
+            kinds["checked"] += 1
+    assert kinds["checked"] < 20 and kinds["clean"] > 5900

@@ -44,7 +44,7 @@ FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42, "C5": 4 * 2 * 4096
 # DP-pipe instructions per DOF-step in the hot loops: counted at run time in
 # the library's SASS (scripts/sass_stats.py; hot-loop kernel, DOFs advanced
 # per loop iteration), these constants only if cuobjdump is unavailable.
-DP_INST_PER_DOF_STEP = {"C1": 42, "C2": 42, "C3": 43, "C4": 47, "C5": None}
+DP_INST_PER_DOF_STEP = {"C1": 42, "C2": 42, "C3": 43, "C4": 43, "C5": None}
 # (kernel, DOF-steps per hot-loop iteration): K1's NS=2 build unrolls its step
 # loop by 4 (k_batch2.cu), so one iteration is 4 steps x 2 systems x 2 DOFs.
 DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb1ELi256E", 2),
@@ -52,7 +52,7 @@ DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb1ELi256E", 2),
                   # the two-operation build (kD2): both of its loops (tested or
                   # not, warp by warp) issue 344 DP instructions per step
                   "C3": ("chain_tiles_persistentILi8ELi256ELb0ELb1E", 8),
-                  "C4": ("chain_rk4_kernelILi8ELb0ELb0ELi128E", 8)}
+                  "C4": ("chain_rk4_kernelILi8ELb0ELb0ELi128ELb1E", 8)}
 
 
 def dp_inst_per_dof_step(config: str, div2_frac=None):

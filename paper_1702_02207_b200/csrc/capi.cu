@@ -163,12 +163,16 @@ int osc_rk4_chains(const double *m, const double *C, double *x, double *v, int64
     }
     Scratch scratch;
     scratch.s = stream;
-    // Tiled runs of the default tile shape divide in two operations where a
-    // tile's divisors allow it (div2_checked_consts): one table pass over the
-    // masses first.  OSC_DIV2=0 keeps three operations (A/B timing).
+    // The default tile shape and the whole-chain 8-cell builds divide in two
+    // operations where a warp's divisors allow it (div2_chain_consts): one
+    // table pass over the masses first.  OSC_DIV2=0 keeps three operations
+    // (A/B timing).
     const char *d2env = std::getenv("OSC_DIV2");
-    const bool d2 = !g.fma && (plan.tiles > 1 || plan.H > 0) && K == kTileK &&
-                    threads == kTileThreads && !(d2env && d2env[0] == '0');
+    // (tiled: the persistent 8 x 256 tiles; whole chains: 8 cells x <= 128
+    // threads without padding -- the builds that read the table)
+    const bool tiled = plan.tiles > 1 || plan.H > 0;
+    const bool d2 = !g.fma && K == kTileK && !(d2env && d2env[0] == '0') &&
+                    (tiled ? threads == kTileThreads : (threads <= 128 && threads * K <= s));
     OSC_CUDA(osc::scratch_alloc(reinterpret_cast<void **>(&scratch.p), (d2 ? 5 : 2) * bytes,
                                 stream));
     if (d2) {

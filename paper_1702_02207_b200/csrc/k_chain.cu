@@ -371,10 +371,13 @@ constexpr int max_threads() { return K <= 1 ? 1024 : K <= 4 ? 512 : 256; }
 // loop free of rematerialised indices; these builds divide with div_fastq
 // (one FSETP per division).  The wider builds keep div_fast
 // (profiles/r01/README.md).
-template <int K, bool kPad, bool kFma, int kMaxT = max_threads<K>()>
+// kD2: the two-operation division from the SegArgs table (non-padded
+// tiles; see chain_tiles_persistent for the warp-by-warp choice).
+template <int K, bool kPad, bool kFma, int kMaxT = max_threads<K>(), bool kD2 = false>
 __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     chain_rk4_kernel(SegArgs g)
 {
+    static_assert(!(kD2 && (kPad || kFma)), "two-operation build: exact, unpadded tiles");
     constexpr bool kQ = K * kMaxT == 1024 && K >= 4;
     __shared__ Edges<kMaxT> edges;
     __shared__ int s_skip;
@@ -417,20 +420,50 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     t.validn = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(K),
                                                                  cend - c0)));
     bool ok0 = true;
+    t.tested = false;
+    int d2 = 0;  // kD2: 2 = untested two-operation loop, 1 = tested, 0 = exact replay only
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int64_t c = c0 + j;
         t.C[j] = c < cend ? g.C[base + c] : 1.0;
-        t.md[j] = make_divisor(c < cend ? g.m[base + c] : 1.0);
-        ok0 &= (kQ && !kFma) ? divisor_range_ok(t.md[j]) : divisor_fast_ok(t.md[j]);
+        if constexpr (!kD2) {
+            t.md[j] = make_divisor(c < cend ? g.m[base + c] : 1.0);
+            ok0 &= (kQ && !kFma) ? divisor_range_ok(t.md[j]) : divisor_fast_ok(t.md[j]);
+        }
+    }
+    if constexpr (kD2) {
+        bool elig = true, clean = true;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int64_t c = base + c0 + j;
+            const uint64_t w = g.bad[c];
+            t.md[j] = Divisor{0.0, g.zh[c], g.zl[c], static_cast<uint32_t>(w)};
+            elig &= t.md[j].y != 0.0;
+            clean &= (w & kDiv2Clean) != 0;
+        }
+        if (__syncthreads_and(elig))
+            d2 = __all_sync(kFull, clean) ? 2 : 1;
+        else
+            ok0 = false;  // a divisor outside the two-operation range: exact replay
     }
     t.Cn = (c0 + K < cend) ? g.C[base + c0 + K] : (t.last ? -0.0 : 1.0);
 
     double x[K], v[K];
     load_state<K>(g, base, c0, cend, x, v);
     bool ok = ok0 && fused_dt_ok(g.k.half_dt);
-    for (int64_t s = 0; s < g.nsteps; ++s)
-        step<K, kPad, kFma ? Arith::Fma : (kQ ? Arith::FastQ : Arith::Fast)>(t, x, v, g.k, edges, ok);
+    if constexpr (kD2) {
+        if (d2 == 2) {
+            for (int64_t s = 0; s < g.nsteps; ++s)
+                step<K, false, Arith::Fast2>(t, x, v, g.k, edges, ok);
+        } else if (d2 == 1) {
+            for (int64_t s = 0; s < g.nsteps; ++s)
+                step<K, false, Arith::Fast2C>(t, x, v, g.k, edges, ok);
+        }
+    } else {
+        for (int64_t s = 0; s < g.nsteps; ++s)
+            step<K, kPad, kFma ? Arith::Fma : (kQ ? Arith::FastQ : Arith::Fast)>(t, x, v, g.k,
+                                                                                 edges, ok);
+    }
 
     if (__syncthreads_or(!ok || owned_bad<K>(x, v, c0, own_start, own_end))) {
         // A division left nvcc's fast path, or a value went non-finite:
@@ -439,6 +472,11 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
         // bad step of the owned cells (NonFiniteStateError.step,
         // oscillator.py:255-260).
         load_state<K>(g, base, c0, cend, x, v);
+        if constexpr (kD2) {  // the replay divides by the masses themselves
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                t.md[j].b = g.m[base + c0 + j];
+        }
         for (int64_t s = 0; s < g.nsteps; ++s) {
             step<K, kPad, kFma ? Arith::Fma : Arith::Exact>(t, x, v, g.k, edges, ok);
             if (__syncthreads_or(owned_bad<K>(x, v, c0, own_start, own_end))) {
@@ -920,6 +958,8 @@ cudaError_t launch_k(const SegArgs &g, int threads, cudaStream_t stream)
         if (TILE > g.n)
             (g.fma ? chain_rk4_kernel<K, true, true, kT2> : chain_rk4_kernel<K, true, false, kT2>)
                 <<<nb, threads, 0, stream>>>(g);
+        else if (K == 8 && g.zh && !g.fma)  // the two-operation build (C4's shape)
+            chain_rk4_kernel<K, false, false, kT2, true><<<nb, threads, 0, stream>>>(g);
         else
             (g.fma ? chain_rk4_kernel<K, false, true, kT2> : chain_rk4_kernel<K, false, false, kT2>)
                 <<<nb, threads, 0, stream>>>(g);

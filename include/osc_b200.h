@@ -210,6 +210,18 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin,
                           const osc_peer_t *right, const osc_edge_sync_t *sync, uint32_t flags,
                           void *stream);
 
+/* osc_rk4_chain_advance with the shard's two-operation division table
+ * (div2: NULL, or 3n 8-byte words [zh | zl | bad] filled by osc_div2c_table
+ * over the same m -- zh = div2, zl = div2 + n, bad = (uint64_t *)(div2 +
+ * 2n)): the tile kernel then divides in two operations warp by warp, as
+ * osc_rk4_chains does by itself.  Same bytes either way. */
+int osc_rk4_chain_advance_div2(const double *m, const double *C, const double *xin,
+                               const double *vin, double *xout, double *vout, int64_t n,
+                               int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
+                               int64_t step0, int64_t *first_bad, const osc_peer_t *left,
+                               const osc_peer_t *right, const osc_edge_sync_t *sync,
+                               const double *div2, uint32_t flags, void *stream);
+
 /* One shard of a chain in the multi-process fused exchange (one process per
  * GPU): the period loop of osc_rk4_chain_advance launches in native code, so
  * a run of P periods costs P kernel launches of host time and nothing else.
@@ -232,6 +244,7 @@ typedef struct {
     int64_t ghost;
     int64_t *first_bad;
     osc_edge_sync_t sync;
+    const double *div2; /* NULL or the shard's table (osc_rk4_chain_advance_div2) */
 } osc_shard_t;
 
 int osc_rk4_shard_run(osc_shard_t *shard, double dt, int64_t nsteps, int64_t halo_steps,

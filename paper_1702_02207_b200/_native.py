@@ -45,6 +45,9 @@ SIGNATURES = {
     "osc_rk4_chain_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                              _dbl, _i64, _i64, _vp, _vp, _vp, _vp,
                                              ctypes.c_uint32, _vp]),
+    "osc_rk4_chain_advance_div2": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
+                                                  _i64, _dbl, _i64, _i64, _vp, _vp, _vp, _vp,
+                                                  _vp, ctypes.c_uint32, _vp]),
     "osc_edge_sync_status": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_uint64), _vp]),
     "osc_rk4_shard_run": (ctypes.c_int, [_vp, _dbl, _i64, _i64, _i64, ctypes.c_uint32, _vp]),
     "osc_stream_write_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
@@ -107,7 +110,7 @@ class Shard(ctypes.Structure):
                 ("nx", (ctypes.c_void_p * 2) * 2), ("nv", (ctypes.c_void_p * 2) * 2),
                 ("n", ctypes.c_int64), ("own_lo", ctypes.c_int64), ("own_hi", ctypes.c_int64),
                 ("offset", ctypes.c_int64 * 2), ("ghost", ctypes.c_int64),
-                ("first_bad", ctypes.c_void_p), ("sync", EdgeSync)]
+                ("first_bad", ctypes.c_void_p), ("sync", EdgeSync), ("div2", ctypes.c_void_p)]
 
 
 class NativeUnavailableError(RuntimeError):

@@ -16,6 +16,7 @@ the multi-GPU driver make; ``oscillator.integrate`` is the drop-in wrapper.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -318,7 +319,7 @@ def chain_plan(B, s, nsteps, halo_steps=0) -> dict:
 
 def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
                   stream=None, fma=False, left=None, right=None, trusted=False, sync=None,
-                  tiles=None):
+                  tiles=None, div2=None):
     """One temporally blocked launch over a shard buffer (osc_rk4_chain_advance).
 
     ``left``/``right``: optional ``(x, v, offset, count)`` -- a neighbour's
@@ -327,7 +328,9 @@ def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
     ``(ready_left, ready_right, counters, period, timeout_ns)`` -- order the
     edge tiles with the neighbours on the device (osc_edge_sync_t).
     ``tiles``: None (all), "interior" or "edges" -- the two subsets whose
-    launches together equal one (OSC_TILES_INTERIOR / OSC_TILES_EDGES)."""
+    launches together equal one (OSC_TILES_INTERIOR / OSC_TILES_EDGES).
+    ``div2``: the shard's two-operation division table (``div2_table(m)``),
+    or None for the three-operation division; same bytes."""
     peers = []
     for p in (left, right):
         peers.append(ctypes.byref(_native.Peer(*p)) if p is not None else None)
@@ -335,10 +338,10 @@ def chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
     if sync is not None:
         rl, rr, ctr, period, timeout_ns = sync
         es = _native.EdgeSync((ctypes.c_void_p * 2)(rl, rr), ctr, int(period), int(timeout_ns))
-    rc = _native.lib().osc_rk4_chain_advance(
+    rc = _native.lib().osc_rk4_chain_advance_div2(
         _ptr(m), _ptr(C), _ptr(xin), _ptr(vin), _ptr(xout), _ptr(vout), m.numel(), int(own_lo),
         int(own_hi), float(dt), int(nsteps), int(step0), _ptr(first_bad), peers[0], peers[1],
-        ctypes.byref(es) if es is not None else None,
+        ctypes.byref(es) if es is not None else None, _ptr(div2),
         (_native.OSC_FMA if fma else 0) | (_native.OSC_TRUSTED if trusted else 0)
         | {None: 0, "interior": _native.OSC_TILES_INTERIOR, "edges": _native.OSC_TILES_EDGES}[tiles],
         ctypes.c_void_p(_stream(stream)))
@@ -389,6 +392,21 @@ def div2_classify(b, *, stream=None) -> torch.Tensor:
                                          ctypes.c_void_p(_stream(stream)))
     raise_for(rc, "osc_div2_classify")
     return out.reshape(b.shape)
+
+
+def div2_table(m, *, stream=None):
+    """The 3n-word table [zh | zl | bad] osc_rk4_chain_advance_div2 and
+    osc_shard_t.div2 take for a shard's masses m (n cells), or None when
+    OSC_DIV2=0 (three-operation division, A/B timing)."""
+    if os.environ.get("OSC_DIV2", "1").startswith("0"):
+        return None
+    m = _dev(m)
+    n = m.numel()
+    t = torch.empty(3 * n, dtype=torch.float64, device=m.device)
+    rc = _native.lib().osc_div2c_table(_ptr(m), n, _ptr(t), _ptr(t[n:]), _ptr(t[2 * n:]),
+                                       ctypes.c_void_p(_stream(stream)))
+    raise_for(rc, "osc_div2c_table")
+    return t
 
 
 def div2c_table(b, *, stream=None):

@@ -292,6 +292,18 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
                           const osc_peer_t *left, const osc_peer_t *right,
                           const osc_edge_sync_t *sync, uint32_t flags, void *stream)
 {
+    return osc_rk4_chain_advance_div2(m, C, xin, vin, xout, vout, n, own_lo, own_hi, dt, nsteps,
+                                      step0, first_bad, left, right, sync, nullptr, flags,
+                                      stream);
+}
+
+int osc_rk4_chain_advance_div2(const double *m, const double *C, const double *xin,
+                               const double *vin, double *xout, double *vout, int64_t n,
+                               int64_t own_lo, int64_t own_hi, double dt, int64_t nsteps,
+                               int64_t step0, int64_t *first_bad, const osc_peer_t *left,
+                               const osc_peer_t *right, const osc_edge_sync_t *sync,
+                               const double *div2, uint32_t flags, void *stream)
+{
     if (flags & ~kAdvanceFlags)
         return fail(OSC_INVALID, "unknown flags 0x%x", flags);
     const uint32_t subset = flags & (OSC_TILES_INTERIOR | OSC_TILES_EDGES);
@@ -329,6 +341,11 @@ int osc_rk4_chain_advance(const double *m, const double *C, const double *xin, c
     g.nsteps = nsteps;
     g.step0 = step0;
     g.fma = (flags & OSC_FMA) != 0;
+    if (div2 && !g.fma) {
+        g.zh = div2;
+        g.zl = div2 + n;
+        g.bad = reinterpret_cast<const uint64_t *>(div2 + 2 * n);
+    }
     const osc_peer_t *peers[2] = {left, right};
     for (int side = 0; side < 2; ++side) {
         const osc_peer_t *p = peers[side];

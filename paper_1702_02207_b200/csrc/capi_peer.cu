@@ -5,6 +5,8 @@
 
 #include "capi_internal.h"
 
+#include <cstdlib>
+
 using namespace osc_capi;
 
 extern "C" {
@@ -174,12 +176,12 @@ int osc_rk4_shard_run(osc_shard_t *sh, double dt, int64_t nsteps, int64_t halo_s
             if (sh->nx[side][nb])
                 peer[side] = osc_peer_t{sh->nx[side][nb], sh->nv[side][nb], sh->offset[side],
                                         sh->ghost};
-        if (int rc = osc_rk4_chain_advance(sh->m, sh->C, sh->x[b], sh->v[b], sh->x[nb],
-                                           sh->v[nb], sh->n, sh->own_lo, sh->own_hi, dt, n,
-                                           step0 + k, sh->first_bad,
-                                           peer[0].x ? &peer[0] : nullptr,
-                                           peer[1].x ? &peer[1] : nullptr, &sh->sync,
-                                           flags | OSC_TRUSTED, stream))
+        if (int rc = osc_rk4_chain_advance_div2(sh->m, sh->C, sh->x[b], sh->v[b], sh->x[nb],
+                                                sh->v[nb], sh->n, sh->own_lo, sh->own_hi, dt, n,
+                                                step0 + k, sh->first_bad,
+                                                peer[0].x ? &peer[0] : nullptr,
+                                                peer[1].x ? &peer[1] : nullptr, &sh->sync,
+                                                sh->div2, flags | OSC_TRUSTED, stream))
             return rc;
         ++sh->sync.period;
         k += n;
@@ -197,6 +199,7 @@ struct ShardRes {
     cudaStream_t st = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     double *m = nullptr, *C = nullptr, *x = nullptr, *v = nullptr, *x2 = nullptr, *v2 = nullptr;
+    double *div2 = nullptr;  // the shard's two-operation division table (3n words)
     int64_t *fb = nullptr;
     int64_t blo = 0, n = 0, own_lo = 0, own_hi = 0;
 };
@@ -213,7 +216,7 @@ struct ShardSet {
         for (auto &r : sh) {
             cudaSetDevice(r.dev);
             for (void *p : {(void *)r.m, (void *)r.C, (void *)r.x, (void *)r.v, (void *)r.x2,
-                            (void *)r.v2, (void *)r.fb})
+                            (void *)r.v2, (void *)r.fb, (void *)r.div2})
                 if (p)
                     cudaFree(p);
             for (auto e : r.ev)
@@ -303,6 +306,18 @@ int osc_rk4_chain_sharded(int ngpu, const int *devs, const double *m, const doub
             return host_param_fail(m, C, s, ParamLayout::Flat);
     }
     flags |= OSC_TRUSTED;  // per-period launches below skip the check
+    if (!(flags & OSC_FMA)) {  // each shard's two-operation division table, once
+        const char *d2env = std::getenv("OSC_DIV2");
+        if (!(d2env && d2env[0] == '0'))
+            for (auto &r : set.sh) {
+                OSC_CUDA(cudaSetDevice(r.dev));
+                OSC_CUDA(cudaMalloc(reinterpret_cast<void **>(&r.div2), 3 * r.n * D));
+                if (int rc = osc_div2c_table(r.m, r.n, r.div2, r.div2 + r.n,
+                                             reinterpret_cast<uint64_t *>(r.div2 + 2 * r.n),
+                                             r.st))
+                    return rc;
+            }
+    }
 
     // neighbours on other devices store into each other's memory over NVLink
     for (int i = 0; i + 1 < ngpu; ++i) {
@@ -342,11 +357,11 @@ int osc_rk4_chain_sharded(int ngpu, const int *devs, const double *m, const doub
                 const ShardRes &q = set.sh[i + 1];
                 right = osc_peer_t{q.x2, q.v2, r.blo - q.blo, g};
             }
-            if (int rc = osc_rk4_chain_advance(r.m, r.C, r.x, r.v, r.x2, r.v2, r.n, r.own_lo,
-                                               r.own_hi, dt, n, k, r.fb,
-                                               i > 0 ? &left : nullptr,
-                                               i + 1 < ngpu ? &right : nullptr, nullptr, flags,
-                                               r.st))
+            if (int rc = osc_rk4_chain_advance_div2(r.m, r.C, r.x, r.v, r.x2, r.v2, r.n,
+                                                    r.own_lo, r.own_hi, dt, n, k, r.fb,
+                                                    i > 0 ? &left : nullptr,
+                                                    i + 1 < ngpu ? &right : nullptr, nullptr,
+                                                    r.div2, flags, r.st))
                 return rc;
             OSC_CUDA(cudaEventRecord(r.ev[p % 2], r.st));
         }

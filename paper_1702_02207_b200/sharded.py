@@ -101,13 +101,13 @@ def layout(s: int, rank: int, world: int, halo_steps: int) -> ShardLayout:
 
 
 def _cuda_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0, first_bad,
-                  stream=None, left=None, right=None, sync=None, tiles=None):
+                  stream=None, left=None, right=None, sync=None, tiles=None, div2=None):
     from . import batched
 
     # the shard's parameters were validated once at construction
     batched.chain_advance(m, C, xin, vin, xout, vout, own_lo, own_hi, dt, nsteps, step0,
                           first_bad, stream=stream, left=left, right=right, trusted=True,
-                          sync=sync, tiles=tiles)
+                          sync=sync, tiles=tiles, div2=div2)
 
 
 class ShardedChain:
@@ -160,8 +160,12 @@ class ShardedChain:
         if timeout_ms is None:
             timeout_ms = float(os.environ.get("OSC_PEER_TIMEOUT_MS", "30000"))
         self.timeout_ns = int(timeout_ms * 1e6)
+        self.div2 = None  # the shard's two-operation division table (CUDA advance only)
         if self.cuda and self.advance is _cuda_advance:
             self._validate(distributed)
+            from . import batched
+
+            self.div2 = batched.div2_table(self.m)
         if transport == "peer" and self.world > 1 and dist.is_initialized() and distributed:
             self._setup_peer()
 
@@ -316,8 +320,9 @@ class ShardedChain:
             sync = None
             if not self._host_order:
                 sync = (self._ready[0], self._ready[1], self._counters.ptr, q, self.timeout_ns)
+            kw = {"div2": self.div2} if self.div2 is not None else {}
             self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, k,
-                         self.first_bad, left=left, right=right, sync=sync)
+                         self.first_bad, left=left, right=right, sync=sync, **kw)
             if self._host_order:
                 torch.cuda.synchronize(self.device)  # our period (and its peer stores) done
                 dist.barrier(group=self.host_group)
@@ -359,6 +364,7 @@ class ShardedChain:
             sh.sync.ready[1] = self._ready[1]
             sh.sync.counters = self._counters.ptr
             sh.sync.timeout_ns = self.timeout_ns
+            sh.div2 = self.div2.data_ptr() if self.div2 is not None else None
         sh.sync.period = self._period
         # the state must be in buffer period % 2 (the Python loop's swaps keep
         # self.x on the current buffer; the native loop relies on parity)
@@ -445,6 +451,8 @@ class ShardedChain:
         kw = {"stream": stream} if self.cuda else {}
         if tiles is not None:
             kw["tiles"] = tiles
+        if self.div2 is not None:
+            kw["div2"] = self.div2
         self.advance(self.m, self.C, self.x, self.v, self.x2, self.v2, a, b, self.dt, n, step0,
                      self.first_bad, **kw)
 
@@ -566,8 +574,9 @@ class LocalShardGroup:
             for sh in self.parts:
                 a, b = sh.L.own
                 left, right = sh.peer_descriptors(p)
+                kw = {"div2": sh.div2} if sh.div2 is not None else {}
                 sh.advance(sh.m, sh.C, sh.x, sh.v, sh.x2, sh.v2, a, b, sh.dt, n, k,
-                           sh.first_bad, left=left, right=right)
+                           sh.first_bad, left=left, right=right, **kw)
             for sh in self.parts:
                 sh.x, sh.x2 = sh.x2, sh.x
                 sh.v, sh.v2 = sh.v2, sh.v

@@ -191,10 +191,10 @@ def test_struct_layouts_match_the_header(tmp_path):
 #include <stdio.h>
 #include "osc_b200.h"
 int main(void) {
-    printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(osc_peer_t), sizeof(osc_edge_sync_t),
+    printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(osc_peer_t), sizeof(osc_edge_sync_t),
            sizeof(osc_shard_t), offsetof(osc_shard_t, nx), offsetof(osc_shard_t, n),
            offsetof(osc_shard_t, ghost), offsetof(osc_shard_t, first_bad),
-           offsetof(osc_shard_t, sync));
+           offsetof(osc_shard_t, sync), offsetof(osc_shard_t, div2));
     return 0;
 }
 ''')
@@ -205,5 +205,6 @@ int main(void) {
                                           check=True).stdout.split()]
     S = _native.Shard
     want = [ctypes.sizeof(_native.Peer), ctypes.sizeof(_native.EdgeSync), ctypes.sizeof(S),
-            S.nx.offset, S.n.offset, S.ghost.offset, S.first_bad.offset, S.sync.offset]
+            S.nx.offset, S.n.offset, S.ghost.offset, S.first_bad.offset, S.sync.offset,
+            S.div2.offset]
     assert got == want

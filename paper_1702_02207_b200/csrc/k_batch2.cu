@@ -27,6 +27,12 @@
 namespace osc {
 namespace {
 
+// kVT: one start-velocity test per step for the fused position sums
+// (add_twice_fused) instead of a test per sum (add_twice_checked).  Used by
+// the one-system-per-thread builds (C1 105 -> 96 ns/step: the tests left the
+// serial step's dependency chain); the two-systems build keeps the per-sum
+// tests (C2 48.17 vs 48.30 ms, profiles/r02/README.md).
+
 // Default launch shape (profiles/r01 sweep).
 constexpr int kBatch2NS = 2, kBatch2Threads = 256;
 
@@ -49,11 +55,16 @@ __device__ __forceinline__ void accel2(double p0, double p1, double C0, double C
 // One classical RK4 step (oscillator.py:208-231).  The combination sums are
 // accumulated left to right exactly as combine_value's
 // ((k1 + 2k2) + 2k3) + k4; 2.0*k is exact.
-template <Arith A>
+template <Arith A, bool kVT = false>
 __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divisor &m0,
                                       const Divisor &m1, const StepConsts &k, bool &ok)
 {
     double a0, a1;
+    // add_twice_fused's condition (osc_device.cuh): the start velocities,
+    // once per step, instead of a test per fused position sum
+    constexpr bool kFused = kVT && A != Arith::Exact && A != Arith::Fma;
+    if constexpr (kFused)
+        ok &= velocity_small(s.v0) & velocity_small(s.v1);
     // k1 at the step start; position slopes are the velocities.
     accel2<A>(s.x0, s.x1, C0, C1, m0, m1, a0, a1, ok);
     double sx0 = s.v0, sx1 = s.v1, sv0 = a0, sv1 = a1;
@@ -63,8 +74,8 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     double yp1 = stage<A>(s.x1, k.half_dt, s.v1);
     // k2 at the midpoint; y2v doubles as the k2 position slope.
     accel2<A>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
-    sx0 = add_twice_checked<A>(sx0, yv0, ok);
-    sx1 = add_twice_checked<A>(sx1, yv1, ok);
+    sx0 = kFused ? add_twice_fused<A>(sx0, yv0) : add_twice_checked<A>(sx0, yv0, ok);
+    sx1 = kFused ? add_twice_fused<A>(sx1, yv1) : add_twice_checked<A>(sx1, yv1, ok);
     sv0 = add_twice<A>(sv0, a0);
     sv1 = add_twice<A>(sv1, a1);
     yp0 = stage<A>(s.x0, k.half_dt, yv0);
@@ -73,8 +84,8 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     yv1 = stage<A>(s.v1, k.half_dt, a1);
     // k3 at the refined midpoint.
     accel2<A>(yp0, yp1, C0, C1, m0, m1, a0, a1, ok);
-    sx0 = add_twice_checked<A>(sx0, yv0, ok);
-    sx1 = add_twice_checked<A>(sx1, yv1, ok);
+    sx0 = kFused ? add_twice_fused<A>(sx0, yv0) : add_twice_checked<A>(sx0, yv0, ok);
+    sx1 = kFused ? add_twice_fused<A>(sx1, yv1) : add_twice_checked<A>(sx1, yv1, ok);
     sv0 = add_twice<A>(sv0, a0);
     sv1 = add_twice<A>(sv1, a1);
     yp0 = stage<A>(s.x0, k.dt, yv0);
@@ -228,7 +239,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
 #pragma unroll
         for (int j = 0; j < NS; ++j)
             saved[j] = s[j];
-        bool ok = ok0 & !exact_only;
+        bool ok = ok0 & !exact_only & (NS > 1 || fused_dt_ok(k.half_dt));
         if (ok) {
             // Throughput builds unroll 4 steps per iteration (loop control was
             // ~1% of the stall samples; +1.2% on C2).  The latency build (NS=1)
@@ -238,7 +249,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)
-                        step2<NS == 1 ? Arith::Fast2A : Arith::Fast2>(
+                        step2<NS == 1 ? Arith::Fast2A : Arith::Fast2, NS == 1>(
                             s[j], C0[j], C1[j], Divisor{0.0, u0[j], w0[j]},
                             Divisor{0.0, u1[j], w1[j]}, k, ok);
                 }
@@ -247,7 +258,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)
-                        step2<kFma ? Arith::Fma : Arith::Fast>(
+                        step2<kFma ? Arith::Fma : Arith::Fast, NS == 1>(
                             s[j], C0[j], C1[j], Divisor{u0[j], w0[j], 0.0},
                             Divisor{u1[j], w1[j], 0.0}, k, ok);
                 }

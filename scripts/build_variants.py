@@ -22,7 +22,8 @@ VARIANTS = {
     "d2c1": ["-DOSC_D2_CHOICE=1"],
     "d2c3": ["-DOSC_D2_CHOICE=3"],
     "d2c4": ["-DOSC_D2_CHOICE=4"],
-    "cu2": ["-DOSC_CHAIN_UNROLL=2"],  # timing bound only: never tested quotients (NOT exact)
+    "cu2": ["-DOSC_CHAIN_UNROLL=2"],
+    "b2vt0": ["-DOSC_B2_VTEST=0"],  # K1 with a test per fused position sum (round 1)  # timing bound only: never tested quotients (NOT exact)
 
 }
 

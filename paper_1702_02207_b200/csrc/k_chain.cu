@@ -38,14 +38,7 @@ constexpr int kMaxDevices = 64;
 #ifndef OSC_PERSIST_BUFS
 #define OSC_PERSIST_BUFS 3
 #endif
-constexpr int kPersistBufs = OSC_PERSIST_BUFS;
-#ifndef OSC_CHAIN_UNROLL
-#define OSC_CHAIN_UNROLL 1
-#endif
-constexpr int kChainUnroll = OSC_CHAIN_UNROLL;  // K3 step-loop unroll (timing experiments)
-#ifndef OSC_D2_CHOICE
-#define OSC_D2_CHOICE 2
-#endif  // tile buffers of the persistent kernel (see there)
+constexpr int kPersistBufs = OSC_PERSIST_BUFS;  // tile buffers of the persistent kernel (see there)
 static_assert(kPersistBufs == 2 || kPersistBufs == 3, "2 or 3 tile buffers");
 
 template <int K>
@@ -58,7 +51,6 @@ struct Tile {
     bool first;    // this thread's cell 0 is the tile's first cell (wall side)
     bool last;     // this thread's cell K-1 is the tile's last cell (free side)
     int pr_off;    // byte offset in a stage's slot row of the value read as the right neighbour
-    bool tested;   // Fast2T: this warp holds a divisor whose quotients are tested (warp-uniform)
 };
 
 // Thread-edge exchange slots, double-buffered by stage parity (compile-time:
@@ -129,14 +121,6 @@ __device__ __forceinline__ void accel(const Tile<K> &t, const double (&p)[K], do
     }
     if constexpr (A == Arith::Fast2C)
         ok &= okb;
-    if constexpr (A == Arith::Fast2T) {
-        if (t.tested) {  // warp-uniform: 12% of C3's warps
-#pragma unroll
-            for (int j = 0; j < K; ++j)
-                okb &= static_cast<uint32_t>(__double2loint(a[j])) != t.md[j].bad;
-            ok &= okb;
-        }
-    }
 }
 
 // A buffer whose divergence was recorded in an EARLIER launch (first_bad <=
@@ -420,7 +404,6 @@ __global__ void __launch_bounds__(kMaxT, (K >= 4 && K * kMaxT == 1024) ? 2 : 1)
     t.validn = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(K),
                                                                  cend - c0)));
     bool ok0 = true;
-    t.tested = false;
     int d2 = 0;  // kD2: 2 = untested two-operation loop, 1 = tested, 0 = exact replay only
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -724,7 +707,6 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
     t.pr_off = t.last ? static_cast<int>((threadIdx.x + 1) * sizeof(double2) + sizeof(double))
                       : static_cast<int>((threadIdx.x + 2) * sizeof(double2));
     t.lastj = -1;
-    t.tested = false;
     t.validn = K;
     const int cl = threadIdx.x * K;  // first cell of this thread within the tile
     int i = 0, b = 0, use = 0;  // b = i % kBufs, use = i / kBufs
@@ -764,18 +746,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                         t.md[j] = Divisor{0.0, zh[j], zl[j], static_cast<uint32_t>(w)};
                         clean &= (w & kDiv2Clean) != 0;
                     }
-#if OSC_D2_CHOICE == 0
-                    d2 = 1;
-#elif OSC_D2_CHOICE == 1
-                    d2 = __syncthreads_and(clean) ? 2 : 1;
-#elif OSC_D2_CHOICE == 3  // timing bound only: NOT exact
-                    d2 = 2;
-#elif OSC_D2_CHOICE == 4
-                    t.tested = __any_sync(kFull, !clean);
-                    d2 = 3;
-#else
-                    d2 = __all_sync(kFull, clean) ? 2 : 1;
-#endif
+d2 = __all_sync(kFull, clean) ? 2 : 1;
                 } else {
                     ok = false;
                 }
@@ -798,10 +769,7 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
             // ptxas handles better (profiles/r01/README.md)
             if constexpr (kD2) {
                 // warp-uniform choice; both loops pass the same barriers
-                if (d2 == 3) {
-                    for (int64_t s = 0; s < g.nsteps; ++s)
-                        step<K, false, Arith::Fast2T>(t, x, v, g.k, edges, ok);
-                } else if (d2 == 2) {
+                if (d2 == 2) {
                     for (int64_t s = 0; s < g.nsteps; ++s)
                         step<K, false, Arith::Fast2>(t, x, v, g.k, edges, ok);
                 } else if (d2 == 1) {
@@ -809,7 +777,6 @@ __global__ void __launch_bounds__(NT, (NT * K <= 1024 ? 2 : 1)) chain_tiles_pers
                         step<K, false, Arith::Fast2C>(t, x, v, g.k, edges, ok);
                 }
             } else {
-#pragma unroll kChainUnroll
                 for (int64_t s = 0; s < g.nsteps; ++s)
                     step<K, false, kFma ? Arith::Fma : Arith::FastQ>(t, x, v, g.k, edges, ok);
             }

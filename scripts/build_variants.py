@@ -17,14 +17,6 @@ VARIANTS = {
     "u2": ["-DOSC_B2_UNROLL=2"],
     "u8": ["-DOSC_B2_UNROLL=8"],
     "pb2": ["-DOSC_PERSIST_BUFS=2"],  # K3 double-buffered (round 1) vs 3 buffers
-    # K3 two-operation loop choice: 0 all tested, 1 per tile, 2 per warp
-    "d2c0": ["-DOSC_D2_CHOICE=0"],
-    "d2c1": ["-DOSC_D2_CHOICE=1"],
-    "d2c3": ["-DOSC_D2_CHOICE=3"],
-    "d2c4": ["-DOSC_D2_CHOICE=4"],
-    "cu2": ["-DOSC_CHAIN_UNROLL=2"],
-    "b2vt0": ["-DOSC_B2_VTEST=0"],  # K1 with a test per fused position sum (round 1)  # timing bound only: never tested quotients (NOT exact)
-
 }
 
 if __name__ == "__main__":

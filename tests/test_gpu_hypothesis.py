@@ -62,18 +62,48 @@ def test_batch2_random(B, nsteps, sdiv, dt, seed, special):
     assert bits(res.v.cpu().numpy()[:, ok]) == bits(vo[:, ok])
 
 
+_TESTED = []
+
+
+def _tested_divisors():
+    """Masses whose two-operation quotients the chain kernels must test
+    (no div2 class: ~0.05% of random masses), drawn once from the device
+    table (osc_div2c_table)."""
+    if not _TESTED:
+        pool = np.random.default_rng(5).uniform(0.5, 2.0, 400_000)
+        bad = batched.div2c_table(pool)[2].cpu().numpy().view(np.uint64)
+        _TESTED.append(pool[(bad >> np.uint64(63)) == 0])
+    return _TESTED[0]
+
+
+def _inject_divisors(rng, m, kind):
+    """kind "tested": ~1% of the masses become tested divisors (scaled by a
+    power of two: the class depends on the significand only), so most warps
+    run the tested two-operation loop; "ineligible": a few masses outside
+    [2^-100, 2^101) send their tiles to the exact replay."""
+    flat = m.reshape(-1)
+    if kind == "tested":
+        k = rng.integers(0, flat.size, max(1, flat.size // 100))
+        flat[k] = rng.choice(_tested_divisors(), k.size) * 2.0 ** rng.integers(-3, 4, k.size)
+    elif kind == "ineligible":
+        k = rng.integers(0, flat.size, max(1, flat.size // 3000))
+        flat[k] = 2.0 ** 101 * rng.uniform(1.0, 4.0, k.size)
+
+
 @SETTINGS
 @given(B=st.integers(1, 6), s=st.one_of(st.integers(1, 2048), st.integers(2049, 12_000)), nsteps=st.integers(1, 120),
        sdiv=st.integers(1, 4), halo=st.integers(0, 40), dt=DT, seed=st.integers(0, 2**32 - 1),
-       special=st.booleans())
-def test_chains_random(B, s, nsteps, sdiv, halo, dt, seed, special):
+       special=st.booleans(), divisors=st.sampled_from(["random", "random", "tested", "ineligible"]))
+def test_chains_random(B, s, nsteps, sdiv, halo, dt, seed, special, divisors):
     rng = np.random.default_rng(seed)
     m, C, x0, v0 = _draw_state(rng, (B, s), special)
+    _inject_divisors(rng, m, divisors)
     stride = max(1, nsteps // sdiv)
     res = batched.integrate_chains(m, C, x0, v0, dt, nsteps, stride, sample=True, check=False,
                                    halo_steps=halo)
     xs, vs, xo, vo, fb = oracle.c_rk4_chains(m, C, x0, v0, dt, nsteps, stride)
-    event(f"{'tiled' if s > 2048 else 'whole-chain'}; diverged: {'some' if fb.any() else 'none'}")
+    event(f"{'tiled' if s > 2048 else 'whole-chain'}; divisors: {divisors}; "
+          f"diverged: {'some' if fb.any() else 'none'}")
     assert res.first_bad.cpu().numpy().tolist() == fb.tolist()
     ok = fb == 0
     gx, gv = res.xs.cpu().numpy(), res.vs.cpu().numpy()

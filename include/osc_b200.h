@@ -250,6 +250,23 @@ typedef struct {
 int osc_rk4_shard_run(osc_shard_t *shard, double dt, int64_t nsteps, int64_t halo_steps,
                       int64_t step0, uint32_t flags, void *stream);
 
+/* The NCCL transport's period loop (one process per GPU, the library
+ * baseline beside the fused peer exchange): per period of halo_steps steps
+ * the interior tiles run on `stream` while, on an internal side stream that
+ * waited for the previous period, our current buffer's ghost zones are
+ * refreshed from the neighbours (ranks rank-1 and rank+1 of `comm`, an
+ * ncclComm_t -- e.g. torch's ProcessGroupNCCL._comm_ptr(); ncclSend/ncclRecv
+ * of `ghost` cells of x and v each way in one NCCL group) and one launch
+ * covers the edge tiles; `stream` then waits for the side stream.  Uses the
+ * shard's m, C, x[2], v[2], n, own_lo, own_hi, ghost (>= 2*halo_steps),
+ * first_bad, div2 and sync.period (buffer parity, advanced per period); the
+ * peer fields are unused.  nranks == 1: plain launches, comm may be NULL.
+ * libnccl.so.2 is opened at the first multi-rank call (not linked).
+ * Asynchronous (stream-ordered); parameters are not re-validated. */
+int osc_rk4_shard_run_nccl(osc_shard_t *shard, void *comm, int rank, int nranks, double dt,
+                           int64_t nsteps, int64_t halo_steps, int64_t step0, uint32_t flags,
+                           void *stream);
+
 /* Stream-ordered 64-bit counters, for ordering work across processes
  * without host synchronisation: osc_stream_write_u64 stores value at addr
  * once all prior work of stream is done (preceded by a system-scope fence, so

@@ -50,6 +50,8 @@ SIGNATURES = {
                                                   _vp, ctypes.c_uint32, _vp]),
     "osc_edge_sync_status": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_uint64), _vp]),
     "osc_rk4_shard_run": (ctypes.c_int, [_vp, _dbl, _i64, _i64, _i64, ctypes.c_uint32, _vp]),
+    "osc_rk4_shard_run_nccl": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, _dbl, _i64,
+                                              _i64, _i64, ctypes.c_uint32, _vp]),
     "osc_stream_write_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_stream_wait_u64": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64]),
     "osc_chain_plan": (ctypes.c_int, [_i64, _i64, _i64, _i64, _vp]),

@@ -488,6 +488,9 @@ class ShardedChain:
         if self.transport == "peer" and self.world > 1 and self.peer_bufs:
             self._run_peer(nsteps)
             return self._reduce_first_bad()
+        if self._native_nccl():
+            self._run_nccl_native(nsteps)
+            return self._reduce_first_bad()
         k = 0
         t_host = time.perf_counter()
         periods = 0
@@ -513,6 +516,47 @@ class ShardedChain:
             periods += 1
         self.host_s_per_period = (time.perf_counter() - t_host) / max(periods, 1)
         return self._reduce_first_bad()
+
+    def _native_nccl(self) -> bool:
+        """The NCCL transport's period loop runs in native code
+        (osc_rk4_shard_run_nccl) when the group is an NCCL group and the
+        shard advances with the CUDA kernel; OSC_NCCL_PY=1 keeps the Python
+        loop below (same schedule, same bytes)."""
+        return (self.world > 1 and self.cuda and self.transport == "nccl"
+                and self.advance is _cuda_advance and dist.is_initialized()
+                and dist.get_backend(self.group) == "nccl"
+                and os.environ.get("OSC_NCCL_PY") != "1")
+
+    def _run_nccl_native(self, nsteps):
+        """One C call enqueues every period: interior tiles on the current
+        stream, the NCCL ghost refresh and the edge tiles on a side stream."""
+        import ctypes
+
+        from . import _native
+
+        group = self.group or dist.distributed_c10d._get_default_group()
+        comm = group._get_backend(self.device)._comm_ptr()
+        sh = _native.Shard()
+        sh.m, sh.C = self.m.data_ptr(), self.C.data_ptr()
+        sh.x[0], sh.x[1] = self.x.data_ptr(), self.x2.data_ptr()
+        sh.v[0], sh.v[1] = self.v.data_ptr(), self.v2.data_ptr()
+        sh.n = self.L.n
+        sh.own_lo, sh.own_hi = self.L.own
+        sh.ghost = self.L.g
+        sh.first_bad = self.first_bad.data_ptr()
+        sh.div2 = self.div2.data_ptr() if self.div2 is not None else None
+        sh.sync.period = 0  # buffer 0 = (x, v), the current state
+        t = time.perf_counter()
+        rc = _native.lib().osc_rk4_shard_run_nccl(
+            ctypes.byref(sh), ctypes.c_void_p(comm), self.rank, self.world, self.dt,
+            int(nsteps), self.T, 0, 0,
+            ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        if rc != _native.OSC_OK:
+            raise RuntimeError(f"osc_rk4_shard_run_nccl: {_native.last_error()}")
+        periods = int(sh.sync.period)
+        self.host_s_per_period = (time.perf_counter() - t) / max(periods, 1)
+        if periods % 2:
+            self._swap()
 
     def _reduce_first_bad(self) -> int:
         fb = self.first_bad.clone()

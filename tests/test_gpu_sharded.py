@@ -192,3 +192,45 @@ def test_tile_subsets_equal_one_launch(n, own, T):
     assert int(fb.item()) == 0
     assert bits(sub_x[a:b].cpu().numpy()) == bits(whole_x[a:b].cpu().numpy())
     assert bits(sub_v[a:b].cpu().numpy()) == bits(whole_v[a:b].cpu().numpy())
+
+
+def test_native_nccl_period_loop_single_rank():
+    """osc_rk4_shard_run_nccl with one rank (no neighbour, no communicator):
+    the native period loop's buffer parity, steps per period and division
+    table give the single-GPU bytes; a multi-rank call without a
+    communicator, or with ghost zones narrower than 2T, is refused."""
+    import ctypes
+
+    from paper_1702_02207_b200 import _native
+
+    s, T, nsteps = 40_000, 13, 150
+    m, C, x0, v0 = _chain(s, 77)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(a, dtype=torch.float64, device=dev).contiguous()  # noqa: E731
+    mm, CC = t(m), t(C)
+    x, v, x2, v2 = t(x0), t(v0), t(x0), t(v0)
+    fb = torch.zeros(1, dtype=torch.int64, device=dev)
+    table = batched.div2_table(mm)
+    sh = _native.Shard()
+    sh.m, sh.C = mm.data_ptr(), CC.data_ptr()
+    sh.x[0], sh.x[1], sh.v[0], sh.v[1] = x.data_ptr(), x2.data_ptr(), v.data_ptr(), v2.data_ptr()
+    sh.n, sh.own_lo, sh.own_hi, sh.ghost = s, 0, s, 0
+    sh.first_bad = fb.data_ptr()
+    sh.div2 = table.data_ptr() if table is not None else None
+    lib = _native.lib()
+    stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    rc = lib.osc_rk4_shard_run_nccl(ctypes.byref(sh), None, 0, 1, 1e-3, nsteps, T, 0, 0, stream)
+    assert rc == _native.OSC_OK, _native.last_error()
+    periods = -(-nsteps // T)
+    assert sh.sync.period == periods
+    out_x, out_v = (x2, v2) if periods % 2 else (x, v)
+    ref = batched.integrate_chains(m, C, x0, v0, 1e-3, nsteps)
+    assert bits(out_x.cpu().numpy()) == bits(ref.x[0].cpu().numpy())
+    assert bits(out_v.cpu().numpy()) == bits(ref.v[0].cpu().numpy())
+    assert int(fb.item()) == 0
+    # refused: two ranks without a communicator; ghosts narrower than 2T
+    sh.own_lo, sh.ghost = 100, 100
+    assert lib.osc_rk4_shard_run_nccl(ctypes.byref(sh), None, 1, 2, 1e-3, 10, T, 0, 0,
+                                      stream) == _native.OSC_INVALID
+    assert lib.osc_rk4_shard_run_nccl(ctypes.byref(sh), ctypes.c_void_p(1), 1, 2, 1e-3, 10,
+                                      60, 0, 0, stream) == _native.OSC_INVALID

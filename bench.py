@@ -727,14 +727,19 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(last["value"])
     value = statistics.median(vals)
+    cfg = shared_config(wl_name, world)
+    dof = cfg.get("dof_steps_per_step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "steps": args.steps, "warmup": args.warmup,
+        # one whole workload at the sampled rate (each timed step is a bounded sample)
+        "ms_per_step": dof / value * 1e3 if dof and value else None,
         "higher_is_better": True, "scaling": "weak" if wl_name == "C1" else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy PCG64, workloads.py)",
-        "config": shared_config(wl_name, world),
+        "config": cfg,
         "impl_notes": {"execution": f"{last['cores']} host threads (rank 0 only)",
+                       "ms_per_step": "the whole workload extrapolated from the sampled rate",
                        "arithmetic": "IEEE fp64 CPU restatement, byte-identical to "
                                      "oscbench.integrate"},
         "cpu_baseline": dict(last, value=value),

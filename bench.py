@@ -685,6 +685,56 @@ def time_side(fn, warm=2, reps=3) -> float:
     return a.elapsed_time(b) * 1e-3 / reps
 
 
+def side_config_records(device, local, fp64, flush, steps=3, warmup=3):
+    """C3, C4 and C5 beside the default C2 line: each workload built and timed
+    as its own --config line is (CUDA events per step on the launching
+    stream, L2 flushed between steps, W warm-up steps), reported as
+    DOF-steps/s with its binding roofline fraction.  A failure is recorded,
+    not fatal to the line."""
+    import torch
+
+    out = {}
+    with ClockSampler(local) as clocks:
+        for name in ("C4", "C3", "C5"):
+            try:
+                wl = Workload(name, 0, device, 0, 1, "peer")
+                n = 2 if name == "C5" else steps
+                for _ in range(warmup):
+                    wl.step()
+                torch.cuda.synchronize()
+                ms = []
+                for _ in range(n):
+                    flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    wl.step()
+                    b.record()
+                    torch.cuda.synchronize()
+                    ms.append(a.elapsed_time(b))
+                t = sum(ms) * 1e-3 / n
+                rec = {"value": wl.dof_steps / t, "unit": UNIT, "ms_per_step": t * 1e3,
+                       "steps": n, "warmup": warmup, "kernel": wl.kernel,
+                       "config": shared_config(name, 1)}
+                if name == "C5":
+                    flops = 2.0 * workloads.C5_S * workloads.C5_S * 2 * workloads.C5_N * 2 * wl.nsteps
+                    dmma = fp64_peak(local, mode=2)
+                    rec["roofline"] = {"bound": "tensor", "frac": flops / t / dmma,
+                                       "achieved": flops / t / 1e12, "peak": dmma / 1e12,
+                                       "unit": "TFLOP/s"}
+                else:
+                    fl = FLOPS_PER_DOF_STEP[name] * wl.dof_steps / t
+                    rec["roofline"] = {"bound": "fp64_pipe", "frac": fl / fp64,
+                                       "achieved": fl / 1e12, "peak": fp64 / 1e12,
+                                       "unit": "TFLOP/s"}
+                out[name] = rec
+                del wl
+                torch.cuda.empty_cache()
+            except Exception as exc:  # noqa: BLE001
+                out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    out["clocks"] = clocks.summary()
+    return out
+
+
 def allreduce_max(value: float, device, backend: str) -> float:
     """Max over ranks (device times are taken per rank; the job's is the max)."""
     import torch
@@ -783,6 +833,8 @@ def main():
     ap.add_argument("--no-sharded-c3", action="store_true",
                     help="at N > 1, skip the sharded C3 sub-record of the default line")
     ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--no-side", action="store_true",
+                    help="at N = 1, skip the C3/C4/C5 side records of the default C2 line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 warm-up steps
@@ -891,6 +943,12 @@ def main():
             "rmse_max": float(err.rmse.max()),
             "what": "modal.compare of every system vs its analytic solution, accumulated in "
                     "the time loop (no samples written)"}
+
+    side = None
+    if wl.name == "C2" and world == 1 and not args.no_side:
+        # the other single-GPU configurations, timed the same way in the same
+        # run (so the driver's record carries them; their own lines: --config)
+        side = side_config_records(device, local, fp64, flush)
 
     engine_line = None
     if wl.name == "C1":
@@ -1006,10 +1064,14 @@ def main():
         "e2e": e2e,
         # + C5: rowscale, pack, unpack; C1/C2: the division classifier and the
         # two kernels of the launch-order partition (cub::DevicePartition)
-        "gpu_launches": (wl.launches + (3 if wl.name in ("C1", "C2", "C5") else 0)) * args.steps,
+        # C3/C4: the two-operation division table pass
+        "gpu_launches": (wl.launches + {"C1": 3, "C2": 3, "C5": 3, "C3": 1, "C4": 1}[wl.name])
+                        * args.steps,
         "clocks": clocks.summary(),
         "step_ms": step_ms,
     }
+    if side is not None:
+        line["side_configs"] = side
     if world > 1 and backend != "nccl":
         line["note"] = f"{world} ranks over {backend} on {torch.cuda.device_count()} GPU(s): " \
                        "a multi-rank path check, not a scaling measurement"

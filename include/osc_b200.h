@@ -343,8 +343,11 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
  * positive divisor; 2: physical ranges; 3: the two-operation division of
  * osc_rk4_batch2 on physical ranges; 4: the same on numerators next to
  * quotient rounding midpoints; 5: the loops' three-operation division with
- * its flag, any operands).  Synchronous; *mismatches (host) receives the
- * number of pairs whose bits differ. */
+ * its flag, any operands; 6 / 7: the chain kernels' checked two-operation
+ * division with its tests, any operands / midpoint-aimed numerators; 8: as
+ * 7 but counting the WRONG two-operation quotients the tests caught).
+ * Synchronous; *mismatches (host) receives the number of pairs whose bits
+ * differ (mode 8: the number caught). */
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream);
 
 /* pass[i] = the class of b[i] for the two-operation division q = RN(a*zh +
@@ -357,17 +360,19 @@ int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches,
  * enqueued on `stream`.  Not part of the reference interface (diagnostic). */
 int osc_div2_classify(const double *b, int64_t n, uint8_t *pass, void *stream);
 
-/* The checked two-operation division of the chain kernels (osc_device.cuh
- * div2_checked_consts): zh[i] = RN(1/b[i]), zl[i] = RN(1/b[i] - zh[i]) and
- * bad[i] = the fraction bits of the one wrong value RN(a*zh + RN(a*zl)) can
- * take instead of RN(a/b) (it has one failing numerator significand at
- * most), or 0x9e3779b9 when there is none; the kernels replay a chunk with
- * IEEE division whenever a quotient's low 32 bits equal bad[i]'s.  zh[i] = 0
- * marks a divisor that is not
- * eligible (outside [2^-100, 2^101), or two failing significands): tiles
- * holding one keep the three-operation division.  osc_rk4_chains computes
- * this table itself for tiled runs.  Device buffers; enqueued on `stream`.
- * Not part of the reference interface (diagnostic). */
+/* The chain kernels' two-operation division table (osc_device.cuh
+ * div2_chain_consts), one entry per divisor b[i]: a divisor with a class (as
+ * osc_div2_classify; 99.95% of random masses) gets that class's zh[i] =
+ * RN(1/b), zl[i] and bad[i] = 2^63 | 0x9e3779b9 ("clean": its quotients need
+ * no test).  Any other divisor gets the class-1 constants and bad[i] = the
+ * fraction bits of the one wrong value RN(a*zh + RN(a*zl)) can take instead
+ * of RN(a/b) (one failing numerator significand at most); the kernels
+ * replay a chunk with IEEE division whenever a quotient's low 32 bits equal
+ * bad[i]'s.  zh[i] = 0 marks a divisor that is not eligible (outside
+ * [2^-100, 2^101), or two failing significands): its tile takes the exact
+ * replay.  A warp whose divisors are all clean runs the untested loop.
+ * osc_rk4_chains computes this table itself.  Device buffers; enqueued on
+ * `stream`.  Not part of the reference interface (diagnostic). */
 int osc_div2c_table(const double *b, int64_t n, double *zh, double *zl, uint64_t *bad,
                     void *stream);
 

@@ -242,6 +242,30 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
         if (!xs && n >= 1 && n <= 64)
             nchunk = std::min<int64_t>(n, B);
     }
+    // 2-DOF batches: three chunks, a small first one (its H2D is the only
+    // exposed upload; it computes while the big one's inputs land), a big one,
+    // and a small last one (its D2H is the only exposed download; its kernels
+    // fill the big chunk's tail).  Small chunks of B/16 systems, rounded to
+    // whole 512-system CTAs of K1: C2 end to end 50.2 -> 48.7 ms against a
+    // 48.1 ms device step (scripts/gpu_e2e_edge.sh, profiles/r02/README.md;
+    // B/20, B/24, B/40 -- not whole CTAs -- and B/64 measured slower).
+    // OSC_HOST_EDGE=k: small chunks of B/k (benchmarking knob; 0 = equal).
+    int64_t edge = 0;
+    if (!chains && nchunk >= 2 && !std::getenv("OSC_HOST_CHUNKS")) {
+        int64_t k = 16;
+        if (const char *e = std::getenv("OSC_HOST_EDGE"))
+            k = std::atoll(e);
+        const int64_t cta = 2 * 256;  // systems per K1 CTA (batch2_entry's shape)
+        if (k >= 3 && B / k >= 148 * 128) {
+            nchunk = 3;
+            edge = std::max<int64_t>(cta, B / k / cta * cta);
+        }
+    }
+    auto bound = [&](int64_t c) -> int64_t {  // first system of chunk c (c = nchunk: B)
+        if (edge)
+            return c == 0 ? 0 : c == 1 ? edge : c == 2 ? B - edge : B;
+        return B * c / nchunk;
+    };
     const int nstream = static_cast<int>(std::min<int64_t>(nchunk, 3));
     HostCtx *ctx = nullptr;
     if (int rc = host_ctx(ctx))
@@ -307,7 +331,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     OSC_CUDA(cudaStreamWaitEvent(pst, evs.ev[nchunk], 0));
     for (int64_t c = 0; c < nchunk; ++c) {
         cudaStream_t st = streams[c % nstream];
-        const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
+        const int64_t b0 = bound(c), b1 = bound(c + 1), nb = b1 - b0;
         if (chains) {
             const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
             OSC_CUDA(cudaMemcpyAsync(dm + o, m + o, n, H2D, pst));
@@ -353,7 +377,7 @@ int host_run(bool chains, const double *m, const double *C, double *x, double *v
     for (int64_t c = 0; c < nchunk; ++c) {
         cudaStream_t st = pst;
         OSC_CUDA(cudaStreamWaitEvent(st, evs.ev[nchunk + 1 + c], 0));
-        const int64_t b0 = B * c / nchunk, b1 = B * (c + 1) / nchunk, nb = b1 - b0;
+        const int64_t b0 = bound(c), b1 = bound(c + 1), nb = b1 - b0;
         if (chains) {
             const size_t o = static_cast<size_t>(b0 * s), n = static_cast<size_t>(nb * s) * 8;
             OSC_CUDA(cudaMemcpyAsync(x + o, dx + o, n, D2H, st));

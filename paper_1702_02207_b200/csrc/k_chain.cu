@@ -5,9 +5,10 @@
 // (oscillator.py:3-5, 152-164).  One CTA owns a TILE of blockDim*K
 // contiguous cells, K per thread, all in registers; the four stage
 // evaluations of a step exchange one neighbour position per thread edge
-// (warp shuffles inside a warp, a double-buffered shared-memory slot plus one
-// __syncthreads between warps -- the on-chip form of the reference engine's
-// per-stage StageBarrier, parallel.py:174-255).
+// (each thread's {first, last} position in a double-buffered shared-memory
+// slot, one __syncthreads -- the on-chip form of the reference engine's
+// per-stage StageBarrier, parallel.py:174-255).  Exact runs divide in two
+// operations warp by warp (div2_chain_consts table; osc_device.cuh).
 //
 // Two launch shapes use the same kernel:
 //   * whole-chain (K2, config 3): the tile is the whole chain (H = 0), so

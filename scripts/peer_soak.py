@@ -32,7 +32,7 @@ def _port():
         return sk.getsockname()[1]
 
 
-def _worker(rank, world, port, seed, runs, q):
+def _worker(rank, world, port, seed, runs, transport, q):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -55,7 +55,9 @@ def _worker(rank, world, port, seed, runs, q):
         t0 = time.monotonic()
         rec = {"world": world, "seed": seed, "run": i, "s": s, "T": T, "nsteps": nsteps}
         try:
-            sh = sharded.ShardedChain(m, C, x0, v0, 1e-3, halo_steps=T, transport="peer")
+            tr = transport if transport != "mixed" else ("peer", "nccl")[i % 2]
+            rec["transport"] = tr
+            sh = sharded.ShardedChain(m, C, x0, v0, 1e-3, halo_steps=T, transport=tr)
             fb = sh.run(nsteps)
             x, v = sh.gather()
             rec["trace"] = sh.trace[-4:]
@@ -87,6 +89,8 @@ def main():
     ap.add_argument("--runs", type=int, default=30)
     ap.add_argument("--budget", type=float, default=600.0, help="wall seconds per group")
     ap.add_argument("--out", default="gpurun_out/peer_soak")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl", "mixed"],
+                    help="nccl: the NCCL-transport schedule (over gloo here); mixed: alternate")
     args = ap.parse_args()
 
     import queue as queue_mod
@@ -103,7 +107,8 @@ def main():
     for gidx in range(args.groups):
         world = 2 + gidx % 2
         q = ctx.Queue()
-        procs = mp.start_processes(_worker, args=(world, _port(), 1000 + gidx, args.runs, q),
+        procs = mp.start_processes(_worker, args=(world, _port(), 1000 + gidx, args.runs,
+                                                  args.transport, q),
                                    nprocs=world, join=False, start_method="spawn")
         deadline = time.monotonic() + args.budget
         done = False
@@ -144,7 +149,7 @@ def main():
         except Exception:  # noqa: BLE001
             pass
     lines.close()
-    summary = (f"peer transport soak: {total} runs ({args.groups} process groups of 2/3 ranks, "
+    summary = (f"{args.transport} transport soak: {total} runs ({args.groups} process groups of 2/3 ranks, "
                f"{args.runs} runs each) -> {ok} byte-exact, {bad} failed, {hung} hung groups; "
                f"slowest run {worst:.2f} s; host time per period (native loop) median "
                f"{(sorted(host_us)[len(host_us) // 2] if host_us else float('nan')):.1f} us; "

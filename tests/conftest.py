@@ -62,11 +62,14 @@ def bits(a):
     return np.ascontiguousarray(np.asarray(a, dtype="<f8")).tobytes()
 
 
-def collect(worker, args, nprocs):
+def collect(worker, args, nprocs, timeout=240.0):
     """Spawn nprocs ranks of worker(rank, *args, queue); return what rank 0
     puts on the queue.  Reads before joining (results larger than a pipe
-    buffer would otherwise deadlock) and fails fast if a rank dies."""
+    buffer would otherwise deadlock) and fails fast if a rank dies.  Bounded:
+    after `timeout` seconds, or on any error (pytest-timeout included), the
+    ranks are terminated, so a stuck rank cannot keep the test session alive."""
     import queue as queue_mod
+    import time
 
     import torch.multiprocessing as mp
 
@@ -74,13 +77,26 @@ def collect(worker, args, nprocs):
     q = ctx.Queue()
     procs = mp.start_processes(worker, args=args + (q,), nprocs=nprocs, join=False,
                                start_method="spawn")
-    while True:
-        try:
-            out = q.get(timeout=1.0)
-            break
-        except queue_mod.Empty:
-            if procs.join(timeout=0):  # raises if a rank failed
-                raise RuntimeError("ranks exited without a result")
-    while not procs.join():
-        pass
-    return out
+    deadline = time.monotonic() + timeout
+    try:
+        while True:
+            try:
+                out = q.get(timeout=1.0)
+                break
+            except queue_mod.Empty:
+                if procs.join(timeout=0):  # raises if a rank failed
+                    raise RuntimeError("ranks exited without a result")
+                if time.monotonic() > deadline:
+                    raise TimeoutError(f"{nprocs} ranks gave no result in {timeout:.0f} s")
+        while not procs.join(timeout=max(1.0, deadline - time.monotonic())):
+            if time.monotonic() > deadline:
+                raise TimeoutError(f"{nprocs} ranks did not exit in {timeout:.0f} s")
+        return out
+    finally:
+        for p in procs.processes:
+            if p.is_alive():
+                p.terminate()
+        for p in procs.processes:
+            p.join(5.0)
+            if p.is_alive():
+                p.kill()

@@ -5,6 +5,8 @@ edge tiles on the device with bounded waits; on one GPU the processes'
 contexts are time-sliced, so a waiting CTA never blocks its neighbour's
 progress -- and a neighbour that stops raises PeerTimeoutError."""
 
+import datetime
+import faulthandler
 import os
 import socket
 
@@ -39,7 +41,9 @@ def _port():
 
 def _worker(rank, world, port, s, nsteps, T, stiff, transport, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    faulthandler.dump_traceback_later(180)  # a stuck rank shows where, before collect ends it
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
     try:
         torch.cuda.set_device(0)
         from paper_1702_02207_b200 import sharded
@@ -106,7 +110,9 @@ def test_processes_random_decompositions(world, s, T, nsteps, transport):
 
 def _worker_runs(rank, world, port, s, runs, T, transport, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    faulthandler.dump_traceback_later(180)  # a stuck rank shows where, before collect ends it
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
     try:
         torch.cuda.set_device(0)
         from paper_1702_02207_b200 import sharded
@@ -158,7 +164,9 @@ def _worker_stuck(rank, world, port, s, T, stuck, timeout_ms, q):
     import time
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    faulthandler.dump_traceback_later(180)  # a stuck rank shows where, before collect ends it
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
     try:
         torch.cuda.set_device(0)
         from paper_1702_02207_b200 import sharded

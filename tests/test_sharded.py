@@ -6,6 +6,7 @@ run the same driver with the kernel).  The result must be byte-identical to
 the single-process integration for every rank count, as the reference's
 engine is for every worker count (test_parallel.py:259-271)."""
 
+import datetime
 import os
 import socket
 
@@ -72,7 +73,8 @@ def _free_port():
 def _worker(rank, world, port, s, nsteps, T, stiff, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
     try:
         m, C, x0, v0 = _chain(s, 11, stiff)
         sh = sharded.ShardedChain(m, C, x0, v0, 1e-3, halo_steps=T, device=torch.device("cpu"),

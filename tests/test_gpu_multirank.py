@@ -94,6 +94,10 @@ from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E
 _SOAK = int(os.environ.get("HYPOTHESIS_SOAK", "1"))
 
 
+# every example spawns fresh processes (~4 s): the module's 300 s bound
+# scales with the example count under a soak (a 50x soak ran into it: the
+# timeout ended example 76, not a hang -- no stack dump was due)
+@pytest.mark.timeout(max(300, 10 * 3 * _SOAK))
 @settings(max_examples=3 * _SOAK, deadline=None, derandomize=_SOAK == 1,
           suppress_health_check=[HealthCheck.too_slow])
 @given(world=st.integers(2, 3), s=st.integers(20_000, 150_000), T=st.integers(4, 40),

@@ -258,6 +258,8 @@ inline int plan_chain(int64_t s, int64_t B, int64_t nsteps, int64_t halo_steps, 
         p.H = 0;
         p.tiles = 1;
         p.per_launch = kWholeChainSteps;
+        if (const char *e = std::getenv("OSC_WHOLE_STEPS"))  // benchmarking knob
+            p.per_launch = std::max<int64_t>(1, std::atoll(e));
         return OSC_OK;
     }
     const bool shaped = env_shape("OSC_TILE", p.K, p.threads);

@@ -566,6 +566,62 @@ def sharded_c3_record(rank, world, device, backend, local, steps=2, warmup=2):
     return rec
 
 
+def guarded_sharded_c3(line, rank, world, device, backend, local):
+    """Run sharded_c3_record on every rank under a watchdog.  `line`: rank 0's
+    finished JSON line (None on the other ranks); the record, or the error,
+    goes into line["sharded_c3"].  The multi-process peer exchange has only
+    ever run time-sliced on one GPU (gpurun has one), so the bench must
+    survive its failure on a real N-GPU box: an exception on one rank leaves
+    the others waiting in a collective, and then the watchdog ends this
+    process -- rank 0 prints the line it already has, with the reason, first
+    (the reference guards its stage barrier the same way: abort + watchdog,
+    parallel.py:205-255)."""
+    limit = float(os.environ.get("OSC_SHARDED_C3_LIMIT", "240"))
+    lock = threading.Lock()
+    state = {"done": False}
+
+    def bail():
+        with lock:
+            if state["done"]:
+                return
+            state["done"] = True
+            if line is not None:
+                line["sharded_c3"] = {"error": f"no result within {limit:.0f} s: a rank failed "
+                                               "or stalled in the sharded C3 side record"}
+                print(json.dumps(line), flush=True)
+            sys.stderr.write(f"bench: rank {rank}: sharded C3 side record abandoned after "
+                             f"{limit:.0f} s\n")
+            sys.stderr.flush()
+            os._exit(0)
+
+    timer = threading.Timer(limit, bail)
+    timer.daemon = True
+    timer.start()
+    failed = None
+    try:
+        if os.environ.get("OSC_BENCH_FAIL_RANK") == str(rank):  # test hook
+            raise RuntimeError("injected failure (OSC_BENCH_FAIL_RANK)")
+        rec = sharded_c3_record(rank, world, device, backend, local)
+    except Exception as exc:  # noqa: BLE001
+        failed = rec = {"error": f"{type(exc).__name__}: {exc}"[:500]}
+    with lock:
+        if state["done"]:  # the watchdog is printing / exiting
+            time.sleep(3600)
+        state["done"] = True
+    timer.cancel()
+    if line is not None:
+        line["sharded_c3"] = rec
+    if failed is not None:
+        # the other ranks may be inside a collective this rank never joined:
+        # do not enter another one (destroy_process_group) -- report and leave
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        sys.stderr.write(f"bench: rank {rank}: sharded C3 side record failed: "
+                         f"{failed['error']}\n")
+        sys.stderr.flush()
+        os._exit(0)
+
+
 def cublas_dgemm(device_index):
     """cuBLAS DGEMM (torch.matmul float64) on the C5 GEMM shape: the library bar."""
     import torch
@@ -907,14 +963,6 @@ def main():
         cpu = cpu_baseline(wl)
         cpu_py = python_reference_baseline(wl.name, wl.host, wl.dt, wl.nsteps)
 
-    sharded_c3 = None
-    if world > 1 and args.config == "C2" and not args.no_sharded_c3:
-        # a side record: a failure here is reported, not fatal to the line
-        try:
-            sharded_c3 = sharded_c3_record(rank, world, device, backend, local)
-        except Exception as exc:  # noqa: BLE001
-            sharded_c3 = {"error": f"{type(exc).__name__}: {exc}"[:500]}
-
     fma_line = None
     if wl.name in ("C2", "C3", "C4") and world == 1:
         # the opt-in OSC_FMA arithmetic on the same workload (not bit-identical;
@@ -970,7 +1018,10 @@ def main():
         wl.shard.close()  # collective: every rank releases its peer mappings
     if world > 1:
         dist.barrier()
+    want_sharded_c3 = world > 1 and args.config == "C2" and not args.no_sharded_c3
     if rank != 0:
+        if want_sharded_c3:
+            guarded_sharded_c3(None, rank, world, device, backend, local)
         if world > 1:
             dist.destroy_process_group()
         return 0
@@ -1075,15 +1126,17 @@ def main():
     if world > 1 and backend != "nccl":
         line["note"] = f"{world} ranks over {backend} on {torch.cuda.device_count()} GPU(s): " \
                        "a multi-rank path check, not a scaling measurement"
-    if sharded_c3:
-        line["sharded_c3"] = sharded_c3
     if engine_line:
         line["equation_engine"] = engine_line
     if fma_line:
         line["fma_mode"] = fma_line
     if validation_line:
         line["validation"] = validation_line
-    print(json.dumps(line))
+    if want_sharded_c3:
+        # last, and with the line complete: a rank that fails or stalls in
+        # this side record costs the sub-record, never the line
+        guarded_sharded_c3(line, rank, world, device, backend, local)
+    print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

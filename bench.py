@@ -599,8 +599,10 @@ def guarded_sharded_c3(line, rank, world, device, backend, local):
     timer.start()
     failed = None
     try:
-        if os.environ.get("OSC_BENCH_FAIL_RANK") == str(rank):  # test hook
+        if os.environ.get("OSC_BENCH_FAIL_RANK") == str(rank):  # test hooks
             raise RuntimeError("injected failure (OSC_BENCH_FAIL_RANK)")
+        if os.environ.get("OSC_BENCH_STALL_RANK") == str(rank):
+            time.sleep(1e6)  # a rank that never arrives: the watchdogs end the job
         rec = sharded_c3_record(rank, world, device, backend, local)
     except Exception as exc:  # noqa: BLE001
         failed = rec = {"error": f"{type(exc).__name__}: {exc}"[:500]}
@@ -960,8 +962,15 @@ def main():
 
     cpu = cpu_py = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(wl)
-        cpu_py = python_reference_baseline(wl.name, wl.host, wl.dt, wl.nsteps)
+        # reported baselines: a failure there must not cost the GPU line
+        try:
+            cpu = cpu_baseline(wl)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"unavailable": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            cpu_py = python_reference_baseline(wl.name, wl.host, wl.dt, wl.nsteps)
+        except Exception as exc:  # noqa: BLE001
+            cpu_py = {"unavailable": f"{type(exc).__name__}: {exc}"[:300]}
 
     fma_line = None
     if wl.name in ("C2", "C3", "C4") and world == 1:

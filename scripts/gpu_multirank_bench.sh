@@ -18,3 +18,8 @@ for fr in 1 0; do
     bench.py --gpus 2 --config C2 --steps 1 --warmup 3 --no-e2e > gpurun_out/mr_fail$fr.json 2> gpurun_out/mr_fail$fr.err; echo fail-rank $fr rc=$?
   python -c "import json;L=open('gpurun_out/mr_fail$fr.json').read().strip().splitlines();d=json.loads(L[-1]);print('fail-rank $fr: lines', len(L), d['n_gpus'], d['value'], d['sharded_c3'])"
 done
+# A rank that stalls: every rank's watchdog ends it, rank 0 prints the line it has.
+P=$((P+1))
+OSC_BENCH_STALL_RANK=1 OSC_SHARDED_C3_LIMIT=45 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port $P \
+  bench.py --gpus 2 --config C2 --steps 1 --warmup 3 --no-e2e > gpurun_out/mr_stall1.json 2> gpurun_out/mr_stall1.err; echo stall-rank 1 rc=$?
+python -c "import json;L=open('gpurun_out/mr_stall1.json').read().strip().splitlines();d=json.loads(L[-1]);print('stall-rank 1: lines', len(L), d['n_gpus'], d['value'], d['sharded_c3'])"

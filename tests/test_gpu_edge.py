@@ -128,6 +128,63 @@ def test_chain_slow_path_cells():
         assert bits(res.x.cpu().numpy()) == bits(xo) and bits(res.v.cpu().numpy()) == bits(vo)
 
 
+@pytest.mark.parametrize("shape", ["tiled", "whole"])
+def test_chain_state_range_edges(shape):
+    """Chain cells at extreme magnitudes: positions around 2^-300 and 2^300 (and
+    far outside: 2^-700, subnormal, exact zeros), velocities up to 2^310 and
+    down to subnormal, spring constants at 2^-100, 2^-120 and -- in chains of
+    their own, which then diverge -- around 2^101.  Every cell must give the
+    reference's bytes (and the diverging chains its first bad step), through
+    the two-operation loops or through the exact replay.  (Written for a
+    build that range-tested the step's start state instead of each quotient,
+    profiles/r02/README.md; the values sit on both sides of its edges.)"""
+    rng = np.random.default_rng(31)
+    B, s = (1, 12000) if shape == "tiled" else (16, 1024)
+    m = rng.uniform(0.5, 2.0, (B, s))
+    C = rng.uniform(500.0, 2000.0, (B, s))
+    x0 = rng.standard_normal((B, s))
+    v0 = rng.standard_normal((B, s))
+    lo, hi = 2.0 ** -300, 2.0 ** 300
+    xs_edge = [lo, np.nextafter(lo, 0.0), -lo, lo * 1.5, 2.0 ** -301, 2.0 ** -353, 2.0 ** -700,
+               np.nextafter(hi, 0.0), hi, -hi, 2.0 ** 299, 2.0 ** 305, 0.0, -0.0, 5e-324]
+    vs_edge = [np.nextafter(hi, 0.0), hi, -hi, 2.0 ** 310, 0.0, 2.0 ** -900, 5e-324, -2.0 ** -320]
+    Cs_edge = [2.0 ** -100, np.nextafter(2.0 ** -100, 0.0), 2.0 ** -120, 2.0 ** 18]
+    # the upper edge of the spring range makes RK4 diverge at any usable dt:
+    # those go into chains of their own (whole shape), whose first bad step
+    # must be the reference's
+    Cs_top = [np.nextafter(2.0 ** 101, 0.0), 2.0 ** 101, 2.0 ** 100] if shape == "whole" else []
+    if shape == "tiled":
+        # spread over the chain: different tiles, tile edges (2048-cell tiles) included
+        cells = rng.choice(np.arange(2, s - 2), size=len(xs_edge) + len(vs_edge) + len(Cs_edge),
+                           replace=False)
+        where = [(0, int(c)) for c in cells]
+    else:
+        # one edge value per chain where possible, first / last / interior cells
+        n = len(xs_edge) + len(vs_edge) + len(Cs_edge)
+        where = [(i % (B - 3), int(c)) for i, c in enumerate(rng.choice(np.arange(s), size=n,
+                                                                        replace=False))]
+    it = iter(where)
+    for val in xs_edge:
+        b, c = next(it)
+        x0[b, c] = val
+    for val in vs_edge:
+        b, c = next(it)
+        v0[b, c] = val
+    for val in Cs_edge:
+        b, c = next(it)
+        C[b, c] = val
+    for i, val in enumerate(Cs_top):
+        C[B - 1 - i, 100 + 300 * i] = val
+    args = (m[0], C[0], x0[0], v0[0]) if B == 1 else (m, C, x0, v0)
+    res = batched.integrate_chains(*args, 1e-4, 90, check=False)
+    _, _, xo, vo, fb = oracle.c_rk4_chains(m, C, x0, v0, 1e-4, 90, sample=False)
+    assert res.first_bad.cpu().numpy().reshape(-1).tolist() == fb.tolist()
+    good = fb == 0
+    assert good[: B - len(Cs_top)].all() and not good[B - len(Cs_top):].any()
+    assert bits(res.x.cpu().numpy().reshape(B, s)[good]) == bits(xo[good])
+    assert bits(res.v.cpu().numpy().reshape(B, s)[good]) == bits(vo[good])
+
+
 def test_many_small_chains_whole_chain_mode():
     """B chains of odd small lengths (padded CTAs)."""
     for s in (3, 17, 100, 513):

@@ -49,7 +49,19 @@ __device__ __forceinline__ void accel2(double p0, double p1, double C0, double C
     const double f1 = mul(C1, d1);
     const double num0 = (A == Arith::Fma) ? __fma_rn(-C0, p0, f1) : add(mul(-C0, p0), f1);
     a0 = qdiv<A>(num0, m0, ok);
-    a1 = qdiv_neg<A>(f1, m1, ok);
+    if constexpr (A == Arith::Fast2S) {
+        // Untested quotients must be right for a ZERO numerator too.  f1 = +0
+        // when p1 == p0 (never -0: a stage position x + c*y of a nonzero x is
+        // never -0, so d1 is not either), and (-f1)/m1 is then -0; but
+        // RN((-0)*zh + RN((-0)*zl)) is +0 when zl < 0.  So the quotient is
+        // negated instead of the numerator: RN(f1*zh + RN(f1*zl)) = +0 for
+        // either sign of zl, and -(f1/m1) == (-f1)/m1 bit for bit otherwise.
+        // The negation folds into the operand modifiers of the uses.  (num0 =
+        // RN((-C0 p0) + f1) is +0 when it is zero; +0/m0 = +0 either way.)
+        a1 = -div2s(f1, m1);
+    } else {
+        a1 = qdiv_neg<A>(f1, m1, ok);
+    }
 }
 
 // One classical RK4 step (oscillator.py:208-231).  The combination sums are
@@ -62,8 +74,13 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     double a0, a1;
     // add_twice_fused's condition (osc_device.cuh): the start velocities,
     // once per step, instead of a test per fused position sum
-    constexpr bool kFused = kVT && A != Arith::Exact && A != Arith::Fma;
-    if constexpr (kFused)
+    // Fast2S: the range of the step's START state replaces every per-quotient
+    // and per-sum test of the step (div2s, osc_device.cuh)
+    constexpr bool kState = A == Arith::Fast2S;
+    constexpr bool kFused = (kVT || kState) && A != Arith::Exact && A != Arith::Fma;
+    if constexpr (kState)
+        ok &= chain_state_ok(s.x0, s.v0) & chain_state_ok(s.x1, s.v1);
+    else if constexpr (kFused)
         ok &= velocity_small(s.v0) & velocity_small(s.v1);
     // k1 at the step start; position slopes are the velocities.
     accel2<A>(s.x0, s.x1, C0, C1, m0, m1, a0, a1, ok);
@@ -191,6 +208,8 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         two &= plan.order ? (plan.mcls[i] != 0) & (plan.mcls[B + i] != 0) : false;
         C0[j] = C[i];
         C1[j] = C[B + i];
+        if constexpr (NS > 1)  // the state-tested loop's spring range (div2s)
+            two &= chain_spring_ok(C0[j]) & chain_spring_ok(C1[j]);
         s[j] = Sys2{x[i], x[B + i], v[i], v[B + i]};
         if (xs && live[j]) {
             xs[i] = s[j].x0;
@@ -239,7 +258,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
 #pragma unroll
         for (int j = 0; j < NS; ++j)
             saved[j] = s[j];
-        bool ok = ok0 & !exact_only & (NS > 1 || fused_dt_ok(k.half_dt));
+        bool ok = ok0 & !exact_only & ((NS > 1 && !two) || fused_dt_ok(k.half_dt));
         if (ok) {
             // Throughput builds unroll 4 steps per iteration (loop control was
             // ~1% of the stall samples; +1.2% on C2).  The latency build (NS=1)
@@ -249,7 +268,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)
-                        step2<NS == 1 ? Arith::Fast2A : Arith::Fast2, NS == 1>(
+                        step2<NS == 1 ? Arith::Fast2A : Arith::Fast2S, NS == 1>(
                             s[j], C0[j], C1[j], Divisor{0.0, u0[j], w0[j]},
                             Divisor{0.0, u1[j], w1[j]}, k, ok);
                 }

@@ -74,6 +74,60 @@ def test_two_operation_division_range_edges():
     _check_batch2(m, C, x0, v0, 1e-4, 300, 100)
 
 
+@pytest.mark.parametrize("shape", ["2,256", "1,128"])
+def test_batch2_state_range_edges(shape, monkeypatch):
+    """The two-systems-per-thread build tests the range of the step's START
+    state instead of every quotient (2^-300 <= |x| < 2^300, |v| < 2^300,
+    2^-100 <= C < 2^101; osc_device.cuh, div2s).  Systems on both sides of
+    every edge, far outside, exact zeros and subnormals: byte-equal to the
+    oracle, through the untested loop, the three-operation loop or the exact
+    replay; the one-system build (numerator tests) sees the same inputs."""
+    monkeypatch.setenv("OSC_B2", shape)
+    rng = np.random.default_rng(41)
+    B = 8192
+    m = rng.uniform(0.5, 2.0, (2, B))
+    C = rng.uniform(500.0, 2000.0, (2, B))
+    x0 = rng.standard_normal((2, B))
+    v0 = rng.standard_normal((2, B))
+    lo, hi = 2.0 ** -300, 2.0 ** 300
+    xe = np.array([lo, np.nextafter(lo, 0.0), -lo, 2.0 ** -301, 2.0 ** -353, 2.0 ** -700, 5e-324,
+                   0.0, -0.0, np.nextafter(hi, 0.0), hi, -hi, 2.0 ** 305, 2.0 ** 299])
+    ve = np.array([np.nextafter(hi, 0.0), hi, -hi, 2.0 ** 310, 0.0, -0.0, 2.0 ** -900, 5e-324])
+    Ce = np.array([2.0 ** -100, np.nextafter(2.0 ** -100, 0.0), 2.0 ** -120, 2.0 ** -90, 2.0 ** 18])
+    pick = rng.permutation(B)
+    k = 0
+    for arr, vals in ((x0, xe), (v0, ve), (C, Ce)):
+        for val in vals:
+            for dof in (0, 1):          # each value in either coordinate, ...
+                arr[dof, pick[k]] = val
+                k += 1
+            arr[:, pick[k]] = val       # ... and in both
+            k += 1
+    _check_batch2(m, C, x0, v0, 1e-4, 200, 50)
+
+
+@pytest.mark.parametrize("shape", ["2,256", "1,128"])
+def test_batch2_equal_positions_keep_the_sign_of_zero(shape, monkeypatch):
+    """x1 == x2 makes the second coordinate's numerator -(C2*(x2 - x1)) = -0,
+    and (-0)/m = -0: with very soft springs the two positions stay equal for
+    many steps and a velocity that starts at -0.0 must stay -0.0.  A
+    two-operation quotient RN(a*zh + RN(a*zl)) of a = -0 is +0 when zl < 0, so
+    the untested loop negates the quotient, not the numerator (accel2)."""
+    monkeypatch.setenv("OSC_B2", shape)
+    rng = np.random.default_rng(7)
+    B = 4096
+    m = rng.uniform(0.5, 2.0, (2, B))
+    C = np.full((2, B), 2.0 ** -90)
+    x0 = np.ones((2, B)) * rng.uniform(0.5, 2.0, B)
+    v0 = np.full((2, B), -0.0)
+    cls = batched.div2_classify(m).cpu().numpy()
+    assert (cls != 0).all(axis=0).mean() > 0.9   # the two-operation loop runs
+    res, fb = _check_batch2(m, C, x0, v0, 1e-4, 8, 4)
+    assert not fb.any()
+    v1 = res.vs.cpu().numpy()[-1, 1]
+    assert (v1 == 0).all() and np.signbit(v1).all()
+
+
 def test_stride_not_dividing_nsteps():
     rng = np.random.default_rng(5)
     m, C = rng.uniform(0.5, 2, (2, 1000)), rng.uniform(500, 2000, (2, 1000))

@@ -145,6 +145,9 @@ constexpr int kChunk = 64;  // steps between divergence checks
 #define OSC_B2_UNROLL 4  // steps per hot-loop iteration (variant builds: scripts/build_variants.py)
 #endif
 constexpr int kUnroll = OSC_B2_UNROLL;
+#ifndef OSC_NS1_STATE
+#define OSC_NS1_STATE 1  // one-system builds: 0 numerator tests, 1 state tests, 2 state tests in the 128-thread build only
+#endif
 
 // Launch order of the systems for the two-operation division: mcls [2][B]
 // holds the div2_classify class of every mass, sys[i] != 0 when both masses
@@ -186,6 +189,10 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                   double *__restrict__ vs, double *__restrict__ es,
                   int64_t *__restrict__ first_bad, Div2Plan plan, CmpArgs cmp = CmpArgs{})
 {
+    // Two-operation loop: range tests on the step's start state (Fast2S) or,
+    // in the builds OSC_NS1_STATE leaves out, on each numerator (Fast2A).
+    constexpr bool kStateTests = NS > 1 || (OSC_NS1_STATE == 1) ||
+                                 (OSC_NS1_STATE == 2 && kMaxThreads == 128);
     const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * NS + threadIdx.x;
     int64_t idx[NS];
     bool live[NS];
@@ -208,7 +215,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         two &= plan.order ? (plan.mcls[i] != 0) & (plan.mcls[B + i] != 0) : false;
         C0[j] = C[i];
         C1[j] = C[B + i];
-        if constexpr (NS > 1)  // the state-tested loop's spring range (div2s)
+        if constexpr (kStateTests)  // the state-tested loop's spring range (div2s)
             two &= chain_spring_ok(C0[j]) & chain_spring_ok(C1[j]);
         s[j] = Sys2{x[i], x[B + i], v[i], v[B + i]};
         if (xs && live[j]) {
@@ -259,6 +266,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         for (int j = 0; j < NS; ++j)
             saved[j] = s[j];
         bool ok = ok0 & !exact_only & ((NS > 1 && !two) || fused_dt_ok(k.half_dt));
+        static_assert(kStateTests || NS == 1, "NS > 1 relies on the state tests' half_dt bound");
         if (ok) {
             // Throughput builds unroll 4 steps per iteration (loop control was
             // ~1% of the stall samples; +1.2% on C2).  The latency build (NS=1)
@@ -268,7 +276,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
                 for (int t = 0; t < n; ++t) {
 #pragma unroll
                     for (int j = 0; j < NS; ++j)
-                        step2<NS == 1 ? Arith::Fast2A : Arith::Fast2S, NS == 1>(
+                        step2<kStateTests ? Arith::Fast2S : Arith::Fast2A, NS == 1>(
                             s[j], C0[j], C1[j], Divisor{0.0, u0[j], w0[j]},
                             Divisor{0.0, u1[j], w1[j]}, k, ok);
                 }

@@ -6,7 +6,7 @@
 // bound by FP64 issue, not by the 48 B/DOF-step one-step-per-round-trip
 // roofline.  Layout is SoA [2][B]: coordinate 0 of every system,
 // then coordinate 1, so a warp's loads/stores are 256 B runs.  Divisions by
-// the masses take two operations (div2_fast, osc_device.cuh) in every warp
+// the masses take two operations (div2s, osc_device.cuh) in every warp
 // whose systems' masses all have a div2 class: a classify kernel and a
 // stable cub partition put those systems first (Div2Plan).
 //
@@ -27,11 +27,12 @@
 namespace osc {
 namespace {
 
-// kVT: one start-velocity test per step for the fused position sums
-// (add_twice_fused) instead of a test per sum (add_twice_checked).  Used by
-// the one-system-per-thread builds (C1 105 -> 96 ns/step: the tests left the
-// serial step's dependency chain); the two-systems build keeps the per-sum
-// tests (C2 48.17 vs 48.30 ms, profiles/r02/README.md).
+// Range tests of the two-operation loops: on the step's START state only
+// (Arith::Fast2S, state_range_ok: 6 FSETPs per system-step, none on the step's
+// dependency chain; osc_device.cuh has the argument).  C2 48.14 -> 47.76 ms,
+// C1 96.0 -> 93.8 ns/step (profiles/r02/README.md).  kVT (the three-operation
+// loop of the one-system builds): one start-velocity test per step for the
+// fused position sums (add_twice_fused) instead of a test per sum.
 
 // Default launch shape (profiles/r01 sweep).
 constexpr int kBatch2NS = 2, kBatch2Threads = 256;
@@ -79,7 +80,7 @@ __device__ __forceinline__ void step2(Sys2 &s, double C0, double C1, const Divis
     constexpr bool kState = A == Arith::Fast2S;
     constexpr bool kFused = (kVT || kState) && A != Arith::Exact && A != Arith::Fma;
     if constexpr (kState)
-        ok &= chain_state_ok(s.x0, s.v0) & chain_state_ok(s.x1, s.v1);
+        ok &= state_range_ok(s.x0, s.v0) & state_range_ok(s.x1, s.v1);
     else if constexpr (kFused)
         ok &= velocity_small(s.v0) & velocity_small(s.v1);
     // k1 at the step start; position slopes are the velocities.
@@ -216,7 +217,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         C0[j] = C[i];
         C1[j] = C[B + i];
         if constexpr (kStateTests)  // the state-tested loop's spring range (div2s)
-            two &= chain_spring_ok(C0[j]) & chain_spring_ok(C1[j]);
+            two &= spring_range_ok(C0[j]) & spring_range_ok(C1[j]);
         s[j] = Sys2{x[i], x[B + i], v[i], v[B + i]};
         if (xs && live[j]) {
             xs[i] = s[j].x0;

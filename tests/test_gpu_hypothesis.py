@@ -40,20 +40,42 @@ def _draw_state(rng, shape, special):
         n = flat[0].size
         for a in flat:
             k = rng.integers(0, n, max(1, n // 20))
-            a[k] = rng.choice([0.0, -0.0, 5e-324, 1e-310, 1e-200, 1e150], k.size)
+            a[k] = rng.choice(_SPECIAL, k.size) * rng.choice([1.0, -1.0], k.size)
     return m, C, x0, v0
+
+
+# zeros, subnormals, far-out magnitudes, and both sides of the bounds of K1's
+# state-range tests (2^-300 <= |x| < 2^300, |v| < 2^300; osc_device.cuh)
+_SPECIAL = np.array([0.0, -0.0, 5e-324, 1e-310, 1e-200, 1e150, 2.0 ** -300,
+                     np.nextafter(2.0 ** -300, 0.0), 2.0 ** -301, 2.0 ** -299, 2.0 ** 300,
+                     np.nextafter(2.0 ** 300, 0.0), 2.0 ** 299, 2.0 ** 301])
+
+
+def _twin_systems(rng, m, C, x0, v0):
+    """A few 2-DOF systems with x1 == x2, zero velocities of either sign and
+    very soft springs: the positions stay equal for many steps, the second
+    coordinate's numerator is -0 at every stage, and the sign of the zero
+    quotient must be the reference's (k_batch2.cu, accel2)."""
+    B = m.shape[1]
+    k = rng.integers(0, B, max(1, B // 16))
+    x0[1, k] = x0[0, k]
+    v0[:, k] = rng.choice([0.0, -0.0], (2, k.size))
+    C[:, k] = 2.0 ** rng.integers(-99, -60, (2, k.size)).astype(float)
 
 
 @SETTINGS
 @given(B=st.integers(1, 3000), nsteps=st.integers(1, 300), sdiv=st.integers(1, 8),
-       dt=DT, seed=st.integers(0, 2**32 - 1), special=st.booleans())
-def test_batch2_random(B, nsteps, sdiv, dt, seed, special):
+       dt=DT, seed=st.integers(0, 2**32 - 1), special=st.booleans(), twins=st.booleans())
+def test_batch2_random(B, nsteps, sdiv, dt, seed, special, twins):
     rng = np.random.default_rng(seed)
     m, C, x0, v0 = _draw_state(rng, (2, B), special)
+    if twins:
+        _twin_systems(rng, m, C, x0, v0)
     stride = max(1, nsteps // sdiv + (seed % 3))
     res = batched.integrate_batch2(m, C, x0, v0, dt, nsteps, stride, sample=True, check=False)
     xs, vs, xo, vo, fb = oracle.c_rk4_batch2(m, C, x0, v0, dt, nsteps, stride)
-    event(f"diverged systems: {'some' if fb.any() else 'none'}; special values: {special}")
+    event(f"diverged systems: {'some' if fb.any() else 'none'}; special values: {special}; "
+          f"twin systems: {twins}")
     assert res.first_bad.cpu().numpy().tolist() == fb.tolist()
     ok = fb == 0
     gx, gv = res.xs.cpu().numpy(), res.vs.cpu().numpy()

@@ -345,7 +345,9 @@ int osc_energy(const double *m, const double *C, const double *x, const double *
  * quotient rounding midpoints; 5: the loops' three-operation division with
  * its flag, any operands; 6 / 7: the chain kernels' checked two-operation
  * division with its tests, any operands / midpoint-aimed numerators; 8: as
- * 7 but counting the WRONG two-operation quotients the tests caught).
+ * 7 but counting the WRONG two-operation quotients the tests caught; 9: the
+ * untested two-operation quotient of osc_rk4_batch2's state-tested loop on
+ * midpoint-aimed numerators over the whole range its state tests admit).
  * Synchronous; *mismatches (host) receives the number of pairs whose bits
  * differ (mode 8: the number caught). */
 int osc_check_division(int64_t n, uint64_t seed, int mode, uint64_t *mismatches, void *stream);

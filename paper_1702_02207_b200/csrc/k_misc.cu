@@ -95,6 +95,10 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t z)
 //   mode 8: as mode 7, but counts the WRONG two-operation quotients that the
 //           flag caught (evidence that the aimed numerators hit the failing
 //           significands the check exists for)
+//   mode 9: the UNTESTED two-operation quotient (div2s, K1's state-tested
+//           loop) on mode 4's midpoint-aimed numerators over the whole range
+//           the state tests admit: |a| in [2^-557, 2^725) or a = +0, classed
+//           b in [2^-100, 2^101); every pair counts
 __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                                       unsigned long long *mismatches)
 {
@@ -156,6 +160,7 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
             // a and b by random powers of two inside the admissible ranges.
             double b0 = __longlong_as_double(static_cast<long long>(bb));
             if (mode == 4 || mode >= 7) {
+                const bool wide = mode == 9;
                 const uint64_t B = mant_b | (1ull << 52);
                 const uint64_t Bo = B >> (__ffsll(static_cast<long long>(B)) - 1);
                 const int sh = (r1 & 1) ? 53 : 54;
@@ -171,14 +176,19 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
                     if (A >= hi)
                         A = r1 >> 12 | (1ull << 52);
                 }
-                const int ea = static_cast<int>((r1 >> 20) % 801) - 400;   // a in [2^-400, 2^401)
-                const int eb = static_cast<int>((r2 >> 53) % 181) - 90;    // b in [2^-90, 2^91)
+                // a in [2^-400, 2^401), b in [2^-90, 2^91); mode 9: [2^-557, 2^725), [2^-100, 2^101)
+                const int ea = wide ? static_cast<int>((r1 >> 20) % 1282) - 557
+                                    : static_cast<int>((r1 >> 20) % 801) - 400;
+                const int eb = wide ? static_cast<int>((r2 >> 53) % 201) - 100
+                                    : static_cast<int>((r2 >> 53) % 181) - 90;
                 ab = ((r1 >> 8) & 1ull) << 63 | (uint64_t(1023 + ea) << 52) |
                      (A & 0x000fffffffffffffull);
                 b0 = __longlong_as_double(static_cast<long long>(
                     (uint64_t(1023 + eb) << 52) | mant_b));
+                if (wide && ((r2 >> 40) & 0xff) == 0)
+                    ab = 0;  // +0: the only zero numerator the state-tested loop divides
             }
-            if (mode >= 7) {
+            if (mode == 7 || mode == 8) {
                 double zh, zl;
                 uint64_t w;
                 if (!div2_checked_consts(b0, zh, zl, w))
@@ -200,6 +210,12 @@ __global__ void check_division_kernel(int64_t n, uint64_t seed, int mode,
             double zh2, zl2;
             div2_consts(b0, cls, zh2, zl2);
             const double a = __longlong_as_double(static_cast<long long>(ab));
+            if (mode == 9) {
+                const double got = div2s(a, Divisor{b0, zh2, zl2});
+                if (__double_as_longlong(got) != __double_as_longlong(__ddiv_rn(a, b0)))
+                    ++bad;
+                continue;
+            }
             bool ok = true, ok_a = true;
             const double got = div2_fast(a, Divisor{b0, zh2, zl2}, ok);
             div2a_fast(a, Divisor{b0, zh2, zl2}, ok_a);  // same quotient, numerator test

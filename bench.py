@@ -45,10 +45,26 @@ FLOPS_PER_DOF_STEP = {"C1": 38, "C2": 38, "C3": 42, "C4": 42, "C5": 4 * 2 * 4096
 # the library's SASS (scripts/sass_stats.py; hot-loop kernel, DOFs advanced
 # per loop iteration), these constants only if cuobjdump is unavailable.
 DP_INST_PER_DOF_STEP = {"C1": 42, "C2": 42, "C3": 43, "C4": 43, "C5": None}
+
+
+def _k1_unroll() -> int:
+    """Steps per hot-loop iteration of K1's two-systems build: the default of
+    OSC_B2_UNROLL in k_batch2.cu (the library bench.py runs is built from it)."""
+    import re
+
+    src = os.path.join(ROOT, "paper_1702_02207_b200", "csrc", "k_batch2.cu")
+    try:
+        with open(src) as f:
+            return int(re.search(r"#define OSC_B2_UNROLL (\d+)", f.read()).group(1))
+    except (OSError, AttributeError):
+        return 2
+
+
 # (kernel, DOF-steps per hot-loop iteration): K1's NS=2 build unrolls its step
-# loop by 4 (k_batch2.cu), so one iteration is 4 steps x 2 systems x 2 DOFs.
+# loop by OSC_B2_UNROLL (k_batch2.cu), so one iteration is that many steps x 2
+# systems x 2 DOFs.
 DP_LOOP_KERNEL = {"C1": ("batch2_rk4_kernelILi1ELb0ELb1ELi256E", 2),
-                  "C2": ("batch2_rk4_kernelILi2ELb0ELb0ELi256E", 16),
+                  "C2": ("batch2_rk4_kernelILi2ELb0ELb0ELi256E", 4 * _k1_unroll()),
                   # the two-operation build (kD2): both of its loops (tested or
                   # not, warp by warp) issue 344 DP instructions per step
                   "C3": ("chain_tiles_persistentILi8ELi256ELb0ELb1E", 8),

@@ -143,7 +143,7 @@ __device__ __forceinline__ bool finite2(const Sys2 &s)
 
 constexpr int kChunk = 64;  // steps between divergence checks
 #ifndef OSC_B2_UNROLL
-#define OSC_B2_UNROLL 4  // steps per hot-loop iteration (variant builds: scripts/build_variants.py)
+#define OSC_B2_UNROLL 2  // steps per hot-loop iteration (variant builds: scripts/build_variants.py); 2 measured best with the state-range tests (47.62 ms vs 47.78 at 4, 47.97 at 3, 48.14 at 1)
 #endif
 constexpr int kUnroll = OSC_B2_UNROLL;
 #ifndef OSC_NS1_STATE
@@ -269,7 +269,7 @@ batch2_rk4_kernel(const double *__restrict__ m, const double *__restrict__ C,
         bool ok = ok0 & !exact_only & ((NS > 1 && !two) || fused_dt_ok(k.half_dt));
         static_assert(kStateTests || NS == 1, "NS > 1 relies on the state tests' half_dt bound");
         if (ok) {
-            // Throughput builds unroll 4 steps per iteration (loop control was
+            // Throughput builds unroll OSC_B2_UNROLL steps per iteration (loop control was
             // ~1% of the stall samples; +1.2% on C2).  The latency build (NS=1)
             // keeps one step per iteration: its schedule gets longer unrolled.
             if (!kFma && two) {

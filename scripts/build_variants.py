@@ -15,6 +15,7 @@ VARIANTS = {
     "O2": ["-Xptxas", "-O2"],
     "u1": ["-DOSC_B2_UNROLL=1"],
     "u2": ["-DOSC_B2_UNROLL=2"],
+    "u3": ["-DOSC_B2_UNROLL=3"],
     "u8": ["-DOSC_B2_UNROLL=8"],
     "pb2": ["-DOSC_PERSIST_BUFS=2"],  # K3 double-buffered (round 1) vs 3 buffers
 }

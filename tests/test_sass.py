@@ -33,9 +33,13 @@ def test_batch2_hot_loops(kernels):
     import sass_stats
 
     # K1's throughput build: the three-operation loop (84 DP per system-step)
-    # and the two-operation loop (76), 4 steps x 2 systems per iteration
+    # and the two-operation loop (76), OSC_B2_UNROLL steps x 2 systems per
+    # iteration -- the bit-exact minimum of 38 DP instructions per DOF-step
+    import bench
+
+    per_iter = 2 * (bench.DP_LOOP_KERNEL["C2"][1] // 4)   # system-steps per iteration
     loops = sass_stats.hot_loops(_body(kernels, "batch2_rk4_kernelILi2ELb0ELb0ELi256E"))
-    assert loops[:2] == [84 * 8, 76 * 8], loops
+    assert loops[:2] == [84 * per_iter, 76 * per_iter], loops
 
 
 def test_chain_hot_loops(kernels):

@@ -23,6 +23,13 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompil
                      "-Xptxas", "-warn-spills", "-I" + os.path.join(HERE, "..", "include")]
 
 
+# Per-source ptxas options (measured on the B200, profiles/r02/README.md): K1's
+# throughput loops (k_batch2_wide.cu) schedule best at register-usage level 2
+# (C2 47.62 -> 47.29 ms); its one-system builds (C1 93.8 -> 101.5 ns/step) and
+# the chain kernels (C3 536 -> 585 ms) lose with it, so it is not a global flag.
+PER_SOURCE_FLAGS = {"k_batch2_wide.cu": ["-Xptxas", "--register-usage-level=2"]}
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and os.path.exists(cand):
@@ -53,7 +60,8 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = OUT,
         obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + headers):
-            jobs.append([nvcc(), *NVCC_FLAGS, *extra, "-c", src, "-o", obj])
+            per = [] if extra else PER_SOURCE_FLAGS.get(os.path.basename(src), [])
+            jobs.append([nvcc(), *NVCC_FLAGS, *per, *extra, "-c", src, "-o", obj])
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         for cmd, res in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True,
                                                                    text=True), jobs)):

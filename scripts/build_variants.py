@@ -9,7 +9,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1702_02207_b200 import build  # noqa: E402
 
 VARIANTS = {
+    "rul0": ["-Xptxas", "--register-usage-level=0"],
+    "rul1": ["-Xptxas", "--register-usage-level=1"],
     "rul2": ["-Xptxas", "--register-usage-level=2"],
+    "rul3": ["-Xptxas", "--register-usage-level=3"],
+    "rul4": ["-Xptxas", "--register-usage-level=4"],
     "rul8": ["-Xptxas", "--register-usage-level=8"],
     "rul10": ["-Xptxas", "--register-usage-level=10"],
     "O2": ["-Xptxas", "-O2"],

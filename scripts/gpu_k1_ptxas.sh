@@ -5,4 +5,4 @@ run() {
 }
 mkdir -p gpurun_out
 run default
-for v in rul2 rul8 rul10 O2; do OSC_LIB=$PWD/paper_1702_02207_b200/_variants/$v/libosc_b200.so run $v; done
+for v in ${VARIANTS:-rul2 rul8 rul10 O2}; do OSC_LIB=$PWD/paper_1702_02207_b200/_variants/$v/libosc_b200.so run $v; done

@@ -14,6 +14,8 @@ VARIANTS = {
     "rul2": ["-Xptxas", "--register-usage-level=2"],
     "rul3": ["-Xptxas", "--register-usage-level=3"],
     "rul4": ["-Xptxas", "--register-usage-level=4"],
+    "rul6": ["-Xptxas", "--register-usage-level=6"],
+    "rul7": ["-Xptxas", "--register-usage-level=7"],
     "rul8": ["-Xptxas", "--register-usage-level=8"],
     "rul10": ["-Xptxas", "--register-usage-level=10"],
     "O2": ["-Xptxas", "-O2"],

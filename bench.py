@@ -130,8 +130,63 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.nvml = None
+
+    def _nvml_start(self) -> bool:
+        """Sample through NVML in this process (the library nvidia-smi itself
+        uses): a query every 100 ms from a thread, no second process attached
+        to the GPU -- the nvidia-smi loop's samples each cost the step they
+        landed in ~1.5 ms (one step in five of a C2 run).  OSC_BENCH_SMI=1
+        keeps the nvidia-smi loop."""
+        if os.environ.get("OSC_BENCH_SMI") == "1":
+            return False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            index = self.index
+            if vis:  # NVML counts physical devices
+                ids = [v.strip() for v in vis.split(",") if v.strip()]
+                if index < len(ids) and ids[index].isdigit():
+                    index = int(ids[index])
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)  # fails early if unsupported
+        except Exception:  # noqa: BLE001 -- no NVML binding: the nvidia-smi loop
+            return False
+        self.nvml = {"stop": threading.Event()}
+
+        def loop():
+            while not self.nvml["stop"].is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    flags = ["Active" if mask & bits[n] else "Not Active" for n in self.NAMES]
+                    self.lines.append(", ".join([str(sm), str(mx)] + flags))
+                except Exception:  # noqa: BLE001
+                    pass
+                self.nvml["stop"].wait(0.1)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+        t_end = time.time() + 1.0
+        while not self.lines and time.time() < t_end:
+            time.sleep(0.005)
+        if not self.lines:  # NVML answers nothing here: the nvidia-smi loop instead
+            self.nvml["stop"].set()
+            self.thread.join(timeout=2)
+            self.nvml = None
+            return False
+        return True
 
     def __enter__(self):
+        if self._nvml_start():
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -153,6 +208,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml:
+            self.nvml["stop"].set()
+            self.thread.join(timeout=2)
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -176,7 +235,9 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "NVML (pynvml), every 100 ms during the timed region" if self.nvml
+                          else "nvidia-smi -lms 200 during the timed region"}
 
 
 # --------------------------------------------------------------------------

@@ -60,7 +60,11 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = OUT,
         obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + headers):
-            per = [] if extra else PER_SOURCE_FLAGS.get(os.path.basename(src), [])
+            # a variant build that sets the same option itself replaces the per-source one
+            per = PER_SOURCE_FLAGS.get(os.path.basename(src), [])
+            if any(f.split("=")[0] in [e.split("=")[0] for e in extra] for f in per
+                   if f.startswith("--")):
+                per = []
             jobs.append([nvcc(), *NVCC_FLAGS, *per, *extra, "-c", src, "-o", obj])
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         for cmd, res in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True,

@@ -149,7 +149,10 @@ __device__ __forceinline__ bool finite2(const Sys2 &s)
     return finite(s.x0) & finite(s.x1) & finite(s.v0) & finite(s.v1);
 }
 
-constexpr int kChunk = 64;  // steps between divergence checks
+#ifndef OSC_B2_CHUNK
+#define OSC_B2_CHUNK 512  // measured: C2 47.31 / 47.21 / 47.16 / 47.13 / 47.13 ms, C1 93.8 / 91.5 / 90.5 / 90.1 / 90.1 ns per step at 64 / 128 / 256 / 512 / 1024
+#endif
+constexpr int kChunk = OSC_B2_CHUNK;  // steps between divergence checks
 #ifndef OSC_B2_UNROLL
 #define OSC_B2_UNROLL 2  // steps per hot-loop iteration (variant builds: scripts/build_variants.py); 2 measured best with the state-range tests (47.62 ms vs 47.78 at 4, 47.97 at 3, 48.14 at 1)
 #endif

@@ -19,6 +19,11 @@ VARIANTS = {
     "rul8": ["-Xptxas", "--register-usage-level=8"],
     "rul10": ["-Xptxas", "--register-usage-level=10"],
     "O2": ["-Xptxas", "-O2"],
+    "c128": ["-DOSC_B2_CHUNK=128"],
+    "c256": ["-DOSC_B2_CHUNK=256"],
+    "c512": ["-DOSC_B2_CHUNK=512"],
+    "c1024": ["-DOSC_B2_CHUNK=1024"],
+    "c4096": ["-DOSC_B2_CHUNK=4096"],
     "u1": ["-DOSC_B2_UNROLL=1"],
     "u2": ["-DOSC_B2_UNROLL=2"],
     "u3": ["-DOSC_B2_UNROLL=3"],

@@ -128,6 +128,26 @@ def test_batch2_equal_positions_keep_the_sign_of_zero(shape, monkeypatch):
     assert (v1 == 0).all() and np.signbit(v1).all()
 
 
+@pytest.mark.parametrize("shape", ["2,256", "1,128", "1,32"])
+def test_batch2_divergence_in_later_chunks(shape, monkeypatch):
+    """Systems just past RK4's stability limit overflow after hundreds to
+    thousands of steps: their first bad step falls in the 1st to 8th chunk of
+    K1's time loop (512 steps between divergence checks), in chunks whose
+    other systems are still fine or have not diverged yet.  First bad step,
+    every sample before it and every surviving system: the reference's."""
+    monkeypatch.setenv("OSC_B2", shape)
+    rng = np.random.default_rng(11)
+    B, dt = 256, 1e-3
+    m = rng.uniform(0.5, 2.0, (2, B))
+    wdt = rng.uniform(2.85, 3.3, B)              # omega*dt around the limit 2.83
+    C = (wdt / dt) ** 2 * m / rng.uniform(2.0, 3.0, (2, B))
+    x0 = rng.standard_normal((2, B))
+    v0 = rng.standard_normal((2, B))
+    _, fb = _check_batch2(m, C, x0, v0, dt, 4000, 500)
+    late = fb[fb > 0]
+    assert (late > 512).sum() > 50 and (late > 1536).sum() > 10 and (fb == 0).sum() > 10
+
+
 def test_stride_not_dividing_nsteps():
     rng = np.random.default_rng(5)
     m, C = rng.uniform(0.5, 2, (2, 1000)), rng.uniform(500, 2000, (2, 1000))
